@@ -1,0 +1,171 @@
+/*
+ * tensched_b200.h - C-ABI of the B200-native V(s) scoring path.
+ *
+ * This is the drop-in boundary for the reference package `tensched`
+ * (arXiv 2011.14486 reconstruction).  Every entry point takes plain
+ * pointers and sizes; device memory is owned by the context; host buffers
+ * are borrowed for the duration of the call.  Results never depend on the
+ * batch size or on how a batch is chunked (value_model.py:33).
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/tensched):
+ *   ts_lstm_forward        <- backend.lstm_forward / _recurrent_cy.lstm_forward
+ *                             (backend.py:26, _recurrent_cy.pyx:20-66)
+ *   ts_featurize_states    <- featurizer.featurize_state + normalize
+ *                             (featurizer.py:68-107, :136-137)
+ *   ts_score_states        <- value_model.predict_states (value_model.py:129-155),
+ *                             the V-callable protocol of search.py:3-8
+ *   ts_candidates          <- schedule_space.candidate_actions (schedule_space.py:379-452)
+ *   ts_greedy              <- search.greedy_schedule (search.py:90-112), fused:
+ *                             candidates -> featurize -> V -> (noise) -> argmin per layer
+ *   ts_params_upload       <- value_model.ValueModelParams / load (value_model.py:37-70, :332-376)
+ *   ts_pipeline_upload     <- pipeline_ir.Pipeline (pipeline_ir.py:116-161) as a flat descriptor
+ *
+ * Errors: every function returns a ts_status; ts_last_error() gives the
+ * message.  The Python layer maps TS_ERR_ILLEGAL to IllegalActionError and
+ * the rest to PipelineError subclasses (pipeline_ir.py:20-37).
+ */
+#ifndef TENSCHED_B200_H
+#define TENSCHED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+#define TS_FEATURE_WIDTH 16 /* featurizer.py:20 */
+#define TS_MAX_PURE 4       /* pure dims per stage */
+#define TS_MAX_RED 4        /* reduction dims per stage */
+#define TS_MAX_LOOPS 8      /* loops per stage after splits */
+#define TS_MAX_STAGES 512
+
+typedef enum ts_status {
+  TS_OK = 0,
+  TS_ERR_ARG = 1,       /* bad argument / shape */
+  TS_ERR_CUDA = 2,      /* CUDA runtime failure */
+  TS_ERR_PIPELINE = 3,  /* descriptor outside the supported envelope */
+  TS_ERR_ILLEGAL = 4,   /* decision record illegal for its state */
+  TS_ERR_OVERFLOW = 5,  /* integer exceeded 256 bits (invocations etc.) */
+  TS_ERR_SELFTEST = 6,  /* device log2 does not match host libm */
+  TS_ERR_NO_DEVICE = 7, /* no sm_100 device */
+  TS_ERR_STATE = 8      /* call order (no params / no pipeline) */
+} ts_status;
+
+/* One scheduling decision (a LayerSchedule, schedule_space.py:37-56) for
+ * the stage at the matching position of schedule order (consumers first,
+ * pipeline_ir.py:207-213).  16 bytes.
+ *   split[k]  split factor of pure dim k (0 = unsplit)
+ *   order[j]  loop ids outermost first: pure dim k -> 2k (whole or outer),
+ *             2k+1 (inner); reduction dim r -> 8+r; 0xFF pads
+ *   vec       vectorize width; flags bit0 = parallel, bit1 = store_at is
+ *             the compute site (else Root); anchor = compute_at loop level
+ *             in the sole consumer's nest, -1 = Root. */
+typedef struct ts_decision {
+  uint8_t split[TS_MAX_PURE];
+  uint8_t order[TS_MAX_LOOPS];
+  uint8_t n_loops;
+  uint8_t vec;
+  uint8_t flags;
+  int8_t anchor;
+} ts_decision;
+
+#define TS_FLAG_PARALLEL 1u
+#define TS_FLAG_STORE_AT 2u
+
+/* Scoring precision. EXACT: fp64 with the Cython kernel's operation order
+ * (_recurrent_cy.pyx:38-65).  FAST: fp32-accurate tensor-core path
+ * (tcgen05, split-fp16 operands, fp32 TMEM accumulators). */
+#define TS_MODE_EXACT 0
+#define TS_MODE_FAST 1
+
+typedef struct ts_ctx ts_ctx;
+
+int ts_abi_version(void);
+const char* ts_last_error(ts_ctx* ctx);
+
+/* Create a context on `device`; runs the device-log2 self-test against the
+ * host libm (hard part 3) and fails with TS_ERR_SELFTEST on a
+ * mismatch. */
+int ts_ctx_create(int device, ts_ctx** out);
+void ts_ctx_destroy(ts_ctx* ctx);
+
+/* Flat pipeline descriptor (layout documented in DESIGN.md and built by
+ * paper_2011_14486_b200/pipeline.py); returns a pipeline id. */
+int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* pipeline_id);
+
+/* Value-model parameters (value_model.py:37-46), row-major f64:
+ * Wx[16][4H], Wh[H][4H], b[4H], w[H]; normalizer mean/std[16]. */
+int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh,
+                     const double* b, const double* w, double b_out, double target_scale,
+                     const double* norm_mean, const double* norm_std);
+
+/* featurize_state (+ normalize when `normalized`): states are ragged runs of
+ * decisions, state i = records[offsets[i] .. offsets[i+1]).  Output
+ * [n][T][16] f64 (T = n_stages, rows in topological order). Bit-exact. */
+int ts_featurize_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records,
+                        const int64_t* offsets, int64_t n_states, int normalized,
+                        double* out);
+
+/* predict_states: V = exp(raw + target_scale) per state, host buffers. */
+int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records,
+                    const int64_t* offsets, int64_t n_states, int mode, double* out_v);
+
+/* Same with device-resident inputs/outputs (pointers into the context's
+ * device), stream-ordered on the context stream. */
+int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,
+                           const int64_t* d_offsets, int64_t n_states, int64_t n_records,
+                           int mode, double* d_out_v);
+
+/* backend.lstm_forward(X, Wx, Wh, b, w, b_out) -> raw (backend.py:26). */
+int ts_lstm_forward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t F,
+                    const double* Wx, const double* Wh, const double* b, const double* w,
+                    int64_t H, double b_out, int mode, double* raw_out);
+
+/* candidate_actions for the state given by `prefix` (n_prefix decisions). */
+int ts_candidates(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix,
+                  ts_decision* out, int64_t capacity, int64_t* n_out);
+
+/* check_action (schedule_space.py:288-347) for decision `a` after `prefix`:
+ * TS_OK if legal, TS_ERR_ILLEGAL with the violated invariant otherwise. */
+int ts_check_action(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix,
+                    const ts_decision* a);
+
+/* Fused greedy_schedule: returns the n_stages decisions and the visited
+ * candidate count.  epsilon > 0 applies the multiplicative noise of
+ * search.py:104-109 from the splitmix64 stream *rng_state (advanced by one
+ * draw per candidate, exactly as SearchRng). */
+int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
+              ts_decision* out_decisions, int64_t* visited, double* out_best_v);
+
+/* Device-side random partial states (the synthetic sweep generator): state i
+ * walks uniformly over candidate_actions with SearchRng(seed0 + i) after
+ * drawing its depth d = randrange(T) + 1 (search.py:136-142 variant).
+ * Writes ragged records (capacity n_states*T) and n_states+1 offsets into
+ * device buffers; *n_records receives the total. */
+int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
+                              ts_decision* d_records, int64_t* d_offsets, int64_t* n_records);
+
+/* Synchronize the context stream; cudaStream_t of the context (as void*). */
+int ts_sync(ts_ctx* ctx);
+void* ts_stream(ts_ctx* ctx);
+
+/* Number of this library's kernel launches since context creation. */
+int64_t ts_launch_count(ts_ctx* ctx);
+
+/* Kernel-class timing (CUDA events on the context stream around each
+ * launch, for bench.py): classes below; ms[k] = summed duration, counts[k]
+ * = launches since the last reset. */
+#define TS_K_FEATURIZE 0
+#define TS_K_LSTM_EXACT 1
+#define TS_K_LSTM_FAST 2
+#define TS_K_OTHER 3
+#define TS_KCLASSES 4
+int ts_set_timing(ts_ctx* ctx, int on);
+int ts_kernel_times(ts_ctx* ctx, double* ms, int64_t* counts, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,802 @@
+// ts_abi.cu - the C-ABI (include/tensched_b200.h): context, descriptor and
+// parameter upload, scoring entry points and the native greedy driver.
+//
+// The greedy driver (ts_greedy) is the fused replacement of
+// search.greedy_schedule (search.py:90-112): per layer it enumerates the
+// candidates on the host (the integer nest math is tiny), then one stream
+// of kernels featurizes the children, dedups identical rows, runs the exact
+// LSTM from the shared prefix and reduces the argmin; only the winner's
+// index comes back.  Only the winner is "applied" (hard part 7).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ts_core.cuh"
+#include "ts_kernels.cuh"
+#include "ts_lstm_tc.cuh"
+
+using namespace ts;
+
+namespace {
+
+constexpr int64_t DESC_HEADER = 4;
+constexpr int64_t DESC_STAGE_WORDS = 48;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t reserve(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t reserve(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMallocHost(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PipelineSlot {
+  std::unique_ptr<PipelineDesc> h;
+  DevBuf d;          // PipelineDesc
+  DevBuf init_raw;   // [T][16]
+  DevBuf init_norm;  // [T][16]
+  DevBuf pre_exact;  // [(T+1)][72]
+  DevBuf pre_fast;   // fast-path prefix
+  uint64_t rows_version = 0;  // params version the init rows / prefix belong to
+  uint64_t fast_version = 0;
+};
+
+}  // namespace
+
+struct ts_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::vector<std::unique_ptr<PipelineSlot>> pipes;
+  // parameters
+  int hidden = 0;
+  uint64_t params_version = 0;
+  double b_out = 0.0, target_scale = 0.0;
+  DevBuf Wx, Wh, b, w, mean, stdv;
+  DevBuf fast_w;  // packed tensor-core weights
+  // scratch
+  DevBuf status, records, offsets, rows, out, reps, raw, nest, tmp, tmp2;
+  HostBuf h_stage, h_out;
+  int64_t launches = 0;
+  // optional per-kernel-class timing (bench.py): events around launches on
+  // the context stream, resolved at the next host synchronization
+  bool timing = false;
+  struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double kms[TS_KCLASSES] = {0};
+  int64_t kcount[TS_KCLASSES] = {0};
+};
+
+namespace {
+
+int fail(ts_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(ts_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, TS_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TS_CUDA(call)                                       \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call); \
+  } while (0)
+
+#define TS_LAUNCHED()                                          \
+  do {                                                         \
+    ++ctx->launches;                                           \
+    cudaError_t _e = cudaGetLastError();                       \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, "launch"); \
+  } while (0)
+
+#define TS_NEED_DEVICE()                                                        \
+  do {                                                                          \
+    if (ctx->device < 0) return fail(ctx, TS_ERR_NO_DEVICE, "host-only context"); \
+  } while (0)
+
+const char* status_name(int s) {
+  switch (s) {
+    case TS_ERR_ARG: return "bad argument";
+    case TS_ERR_PIPELINE: return "pipeline outside the supported envelope";
+    case TS_ERR_ILLEGAL: return "illegal decision record for its state";
+    case TS_ERR_OVERFLOW: return "integer exceeded 256 bits";
+    default: return "error";
+  }
+}
+
+cudaEvent_t take_event(ts_ctx* ctx) {
+  cudaEvent_t e;
+  if (!ctx->event_pool.empty()) {
+    e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+
+// RAII timer: records start/stop events around one launch when timing is on.
+struct KTimer {
+  ts_ctx* ctx;
+  int cls;
+  cudaEvent_t a = nullptr;
+  KTimer(ts_ctx* c, int k) : ctx(c), cls(k) {
+    if (ctx->timing) {
+      a = take_event(ctx);
+      cudaEventRecord(a, ctx->stream);
+    }
+  }
+  ~KTimer() {
+    if (a) {
+      cudaEvent_t b = take_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->pending.push_back({cls, a, b});
+    }
+  }
+};
+
+void resolve_timers(ts_ctx* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      ctx->kms[p.cls] += ms;
+      ctx->kcount[p.cls] += 1;
+    }
+    ctx->event_pool.push_back(p.a);
+    ctx->event_pool.push_back(p.b);
+  }
+  ctx->pending.clear();
+}
+
+// Reads back and clears the device status word.
+int check_device_status(ts_ctx* ctx) {
+  int st = 0;
+  TS_CUDA(cudaMemcpyAsync(&st, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  resolve_timers(ctx);
+  if (st) {
+    TS_CUDA(cudaMemsetAsync(ctx->status.p, 0, sizeof(int), ctx->stream));
+    return fail(ctx, st, std::string("device: ") + status_name(st));
+  }
+  return TS_OK;
+}
+
+PipelineSlot* get_pipe(ts_ctx* ctx, int id) {
+  if (id < 0 || id >= (int)ctx->pipes.size()) return nullptr;
+  return ctx->pipes[id].get();
+}
+
+LstmW lstm_weights(ts_ctx* ctx) {
+  LstmW W;
+  W.Wx = ctx->Wx.as<double>();
+  W.Wh = ctx->Wh.as<double>();
+  W.b = ctx->b.as<double>();
+  W.w = ctx->w.as<double>();
+  W.H = ctx->hidden;
+  return W;
+}
+
+// Init rows + exact prefix for the current parameters.
+int ensure_pipe_ready(ts_ctx* ctx, PipelineSlot* P) {
+  if (!ctx->params_version) return fail(ctx, TS_ERR_STATE, "no parameters uploaded");
+  if (P->rows_version == ctx->params_version) return TS_OK;
+  const int T = P->h->n_stages;
+  TS_CUDA(P->init_raw.reserve(sizeof(double) * T * F));
+  TS_CUDA(P->init_norm.reserve(sizeof(double) * T * F));
+  TS_CUDA(P->pre_exact.reserve(sizeof(double) * (T + 1) * 72));
+  k_init_rows<<<(T + 127) / 128, 128, 0, ctx->stream>>>(P->d.as<PipelineDesc>(), ctx->mean.as<double>(),
+                                                       ctx->stdv.as<double>(), P->init_raw.as<double>(),
+                                                       P->init_norm.as<double>());
+  TS_LAUNCHED();
+  k_prefix_exact<<<1, 32, 0, ctx->stream>>>(lstm_weights(ctx), P->init_norm.as<double>(), T,
+                                            ctx->b_out, P->pre_exact.as<double>());
+  TS_LAUNCHED();
+  P->rows_version = ctx->params_version;
+  return TS_OK;
+}
+
+int self_test(ts_ctx* ctx) {
+  // Values: all ints in [1, 2^16], known non-correctly-rounded ints, and a
+  // spread of doubles; compare device glibc_log2 and the host port against
+  // the host libm log2 bit for bit.
+  std::vector<double> xs;
+  for (int i = 1; i <= 65536; ++i) xs.push_back((double)i);
+  const double extra[] = {1621.0, 3242.0, 57803.0, 0.999, 1.0001, 1.5, 0.75, 3.0e-3, 1.0e30, 2.0e40};
+  for (double e : extra) xs.push_back(e);
+  uint64_t st = 0x1234567ull;
+  for (int i = 0; i < 16384; ++i) {
+    const uint64_t z = splitmix_next(st);
+    const double u = (double)(z >> 11) * 1.1102230246251565e-16;
+    xs.push_back(std::exp2(u * 120.0 - 20.0));
+    xs.push_back(1.0 + (u - 0.5) * 0.1);
+  }
+  const size_t n = xs.size();
+  for (size_t i = 0; i < n; ++i) {
+    const double want = std::log2(xs[i]);
+    if (as_u64(glibc_log2(xs[i])) != as_u64(want)) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "host log2 port mismatch at %.17g: libm build differs from glibc 2.39",
+               xs[i]);
+      return fail(ctx, TS_ERR_SELFTEST, buf);
+    }
+  }
+  DevBuf dx, dy;
+  TS_CUDA(dx.reserve(n * 8));
+  TS_CUDA(dy.reserve(n * 8));
+  TS_CUDA(cudaMemcpy(dx.p, xs.data(), n * 8, cudaMemcpyHostToDevice));
+  k_log2_selftest<<<(int)((n + 255) / 256), 256>>>(dx.as<double>(), dy.as<double>(), (int64_t)n);
+  TS_LAUNCHED();
+  std::vector<double> ys(n);
+  TS_CUDA(cudaMemcpy(ys.data(), dy.p, n * 8, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) {
+    if (as_u64(ys[i]) != as_u64(std::log2(xs[i]))) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "device log2 mismatch at %.17g", xs[i]);
+      return fail(ctx, TS_ERR_SELFTEST, buf);
+    }
+  }
+  return TS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+const char* ts_last_error(ts_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int ts_ctx_create(int device, ts_ctx** out) {
+  if (!out) return TS_ERR_ARG;
+  *out = nullptr;
+  if (device == -1) {
+    // host-only context: descriptor registry + candidate enumeration and
+    // legality; every device entry point refuses with TS_ERR_NO_DEVICE
+    auto* ctx = new ts_ctx();
+    ctx->device = -1;
+    *out = ctx;
+    return TS_OK;
+  }
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+    return TS_ERR_NO_DEVICE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+    return TS_ERR_NO_DEVICE;
+  auto* ctx = new ts_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbol(d_log2_data, ts_log2_data_bits, sizeof(uint64_t) * TS_LOG2_NDATA);
+  if (e == cudaSuccess) e = ctx->status.reserve(sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(ctx->status.p, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    delete ctx;
+    return TS_ERR_CUDA;
+  }
+  const int rc = self_test(ctx);
+  if (rc) {
+    fprintf(stderr, "tensched_b200: %s\n", ctx->err.c_str());
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return TS_OK;
+}
+
+void ts_ctx_destroy(ts_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->device < 0) {
+    delete ctx;
+    return;
+  }
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->pipes.clear();
+  cudaStream_t s = ctx->stream;
+  delete ctx;
+  if (s) cudaStreamDestroy(s);
+}
+
+int ts_set_timing(ts_ctx* ctx, int on) {
+  if (!ctx) return TS_ERR_ARG;
+  ctx->timing = on != 0;
+  return TS_OK;
+}
+
+int ts_kernel_times(ts_ctx* ctx, double* ms, int64_t* counts, int reset) {
+  if (!ctx || !ms || !counts) return TS_ERR_ARG;
+  if (ctx->device >= 0) {
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+    resolve_timers(ctx);
+  }
+  for (int k = 0; k < TS_KCLASSES; ++k) {
+    ms[k] = ctx->kms[k];
+    counts[k] = ctx->kcount[k];
+    if (reset) {
+      ctx->kms[k] = 0.0;
+      ctx->kcount[k] = 0;
+    }
+  }
+  return TS_OK;
+}
+
+int ts_sync(ts_ctx* ctx) {
+  if (!ctx) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
+void* ts_stream(ts_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int64_t ts_launch_count(ts_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* pipeline_id) {
+  if (!ctx || !desc || !pipeline_id) return TS_ERR_ARG;
+  if (n_words < DESC_HEADER || desc[0] != 0x54534231 /* "TSB1" */)
+    return fail(ctx, TS_ERR_ARG, "bad descriptor header");
+  const int64_t T = desc[1], n_slots = desc[2];
+  if (T < 1 || T > TS_MAX_STAGES) return fail(ctx, TS_ERR_PIPELINE, "stage count outside 1..512");
+  if (n_slots < 0 || n_slots > MAX_SLOTS)
+    return fail(ctx, TS_ERR_PIPELINE, "too many simultaneously live nests (max 16)");
+  if (n_words != DESC_HEADER + T * DESC_STAGE_WORDS) return fail(ctx, TS_ERR_ARG, "descriptor size");
+  auto slot = std::make_unique<PipelineSlot>();
+  slot->h = std::make_unique<PipelineDesc>();
+  PipelineDesc& P = *slot->h;
+  memset(&P, 0, sizeof(P));
+  P.n_stages = (int32_t)T;
+  P.n_slots = (int32_t)n_slots;
+  for (int64_t s = 0; s < T; ++s) {
+    const int64_t* w = desc + DESC_HEADER + s * DESC_STAGE_WORDS;
+    StageDesc& sd = P.st[s];
+    sd.n_pure = (int32_t)w[0];
+    sd.n_red = (int32_t)w[1];
+    if (sd.n_pure < 1 || sd.n_pure > TS_MAX_PURE || sd.n_red < 0 || sd.n_red > TS_MAX_RED)
+      return fail(ctx, TS_ERR_PIPELINE, "stage dims outside 1..4 pure / 0..4 reduction");
+    for (int k = 0; k < 8; ++k) sd.ext[k] = w[2 + k];
+    sd.pure_points = (uint64_t)w[10];
+    sd.red_points = (uint64_t)w[11];
+    sd.domain_points = (uint64_t)w[12];
+    sd.i_points = (uint64_t)w[13];
+    sd.i_flops = (uint64_t)w[14];
+    sd.i_in_bytes = (uint64_t)w[15];
+    sd.i_out_bytes = (uint64_t)w[16];
+    sd.n_inputs = (int32_t)w[17];
+    sd.ov_window = (int32_t)w[18];
+    sd.ov_stride = (int32_t)w[19];
+    sd.consumer = (int32_t)w[20];
+    sd.n_cedges = (int32_t)w[21];
+    if (sd.n_cedges < 0 || sd.n_cedges > 2)
+      return fail(ctx, TS_ERR_PIPELINE, "more than 2 parallel edges from the sole consumer");
+    for (int e = 0; e < 2; ++e)
+      for (int k = 0; k < 4; ++k) {
+        sd.cdim[e][k] = (int32_t)w[22 + e * 4 + k];
+        sd.cstride[e][k] = w[30 + e * 4 + k];
+        sd.cwindow[e][k] = w[38 + e * 4 + k];
+      }
+    sd.slot = (int32_t)w[46];
+    sd.n_splittable = (int32_t)w[47];
+    if (sd.consumer >= T || sd.slot >= n_slots || (sd.consumer >= 0 && sd.consumer <= s))
+      return fail(ctx, TS_ERR_PIPELINE, "bad consumer/slot");
+  }
+  for (int64_t s = 0; s < T; ++s)
+    if (P.st[s].consumer >= 0 && P.st[P.st[s].consumer].slot < 0)
+      return fail(ctx, TS_ERR_PIPELINE, "sole consumer without a nest slot");
+  if (ctx->device >= 0) {
+    TS_CUDA(cudaSetDevice(ctx->device));
+    TS_CUDA(slot->d.reserve(sizeof(PipelineDesc)));
+    TS_CUDA(cudaMemcpy(slot->d.p, &P, sizeof(PipelineDesc), cudaMemcpyHostToDevice));
+  }
+  ctx->pipes.push_back(std::move(slot));
+  *pipeline_id = (int)ctx->pipes.size() - 1;
+  return TS_OK;
+}
+
+int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh, const double* b,
+                     const double* w, double b_out, double target_scale, const double* norm_mean,
+                     const double* norm_std) {
+  if (!ctx || !Wx || !Wh || !b || !w || !norm_mean || !norm_std) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (hidden < 1 || hidden > 32) return fail(ctx, TS_ERR_ARG, "hidden size must be in 1..32");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const size_t G = 4 * (size_t)hidden;
+  TS_CUDA(ctx->Wx.reserve(sizeof(double) * F * G));
+  TS_CUDA(ctx->Wh.reserve(sizeof(double) * hidden * G));
+  TS_CUDA(ctx->b.reserve(sizeof(double) * G));
+  TS_CUDA(ctx->w.reserve(sizeof(double) * hidden));
+  TS_CUDA(ctx->mean.reserve(sizeof(double) * F));
+  TS_CUDA(ctx->stdv.reserve(sizeof(double) * F));
+  TS_CUDA(cudaMemcpy(ctx->Wx.p, Wx, sizeof(double) * F * G, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->Wh.p, Wh, sizeof(double) * hidden * G, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->b.p, b, sizeof(double) * G, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->w.p, w, sizeof(double) * hidden, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->mean.p, norm_mean, sizeof(double) * F, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->stdv.p, norm_std, sizeof(double) * F, cudaMemcpyHostToDevice));
+  ctx->hidden = hidden;
+  ctx->b_out = b_out;
+  ctx->target_scale = target_scale;
+  ++ctx->params_version;
+  const int rc = tc_pack_weights(ctx->stream, Wx, Wh, b, w, hidden, &ctx->fast_w.p, &ctx->fast_w.bytes);
+  if (rc) return fail(ctx, rc, "packing tensor-core weights");
+  return TS_OK;
+}
+
+int ts_featurize_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records,
+                        const int64_t* offsets, int64_t n_states, int normalized, double* out) {
+  if (!ctx || !offsets || !out || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  const int T = P->h->n_stages;
+  const int64_t n_rec = offsets[n_states];
+  TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n_rec > 0 ? n_rec : 1)));
+  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
+  TS_CUDA(ctx->out.reserve(sizeof(double) * n_states * T * F));
+  if (n_rec)
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, records, sizeof(ts_decision) * n_rec, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n_states + 1),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  k_featurize_full<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), ctx->records.as<ts_decision>(), ctx->offsets.as<int64_t>(), n_states,
+      P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), normalized,
+      ctx->out.as<double>(), ctx->status.as<int>());
+  TS_LAUNCHED();
+  TS_CUDA(cudaMemcpyAsync(out, ctx->out.p, sizeof(double) * n_states * T * F, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  return check_device_status(ctx);
+}
+
+static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_records,
+                        const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
+                        double* d_out) {
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  const int T = P->h->n_stages;
+  if (mode == TS_MODE_EXACT) {
+    TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1)));
+    KTimer kt0(ctx, TS_K_FEATURIZE);
+    k_featurize_rows<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
+        ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
+    TS_LAUNCHED();
+    const int64_t threads = n_states * 32;
+    KTimer kt1(ctx, TS_K_LSTM_EXACT);
+    k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
+        lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
+        ctx->target_scale, d_out);
+    TS_LAUNCHED();
+    return TS_OK;
+  }
+  if (mode == TS_MODE_FAST) {
+    rc = tc_score_states(ctx->stream, P->d.as<PipelineDesc>(), T, d_records, d_offsets, n_states,
+                         n_records, P->init_raw.as<double>(), P->init_norm.as<double>(),
+                         ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->fast_w.p, ctx->hidden,
+                         ctx->b_out, ctx->target_scale, ctx->params_version, &P->pre_fast.p,
+                         &P->pre_fast.bytes, &P->fast_version, &ctx->tmp.p, &ctx->tmp.bytes,
+                         &ctx->tmp2.p, &ctx->tmp2.bytes, ctx->status.as<int>(), d_out, &ctx->launches);
+    if (rc) return fail(ctx, rc, "fast path");
+    return TS_OK;
+  }
+  return fail(ctx, TS_ERR_ARG, "unknown mode");
+}
+
+int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, const int64_t* offsets,
+                    int64_t n_states, int mode, double* out_v) {
+  if (!ctx || !offsets || !out_v || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t n_rec = offsets[n_states];
+  TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n_rec > 0 ? n_rec : 1)));
+  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
+  TS_CUDA(ctx->out.reserve(sizeof(double) * n_states));
+  if (n_rec)
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, records, sizeof(ts_decision) * n_rec, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n_states + 1),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  int rc = score_device(ctx, P, ctx->records.as<ts_decision>(), ctx->offsets.as<int64_t>(), n_states,
+                        n_rec, mode, ctx->out.as<double>());
+  if (rc) return rc;
+  TS_CUDA(cudaMemcpyAsync(out_v, ctx->out.p, sizeof(double) * n_states, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  return check_device_status(ctx);
+}
+
+int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,
+                           const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
+                           double* d_out_v) {
+  if (!ctx || !d_offsets || !d_out_v || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = score_device(ctx, P, d_records, d_offsets, n_states, n_records, mode, d_out_v);
+  if (rc) return rc;
+  return check_device_status(ctx);
+}
+
+int ts_lstm_forward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t Fdim, const double* Wx,
+                    const double* Wh, const double* b, const double* w, int64_t H, double b_out, int mode,
+                    double* raw_out) {
+  if (!ctx || !X || !raw_out || B < 0 || T < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (Fdim != F) return fail(ctx, TS_ERR_ARG, "feature width must be 16");
+  if (H < 1 || H > 32) return fail(ctx, TS_ERR_ARG, "hidden size must be in 1..32");
+  if (mode != TS_MODE_EXACT) return fail(ctx, TS_ERR_ARG, "lstm_forward supports the exact mode");
+  if (B == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const size_t G = 4 * (size_t)H;
+  // weights travel with the call (backend.py:26 signature); staged in tmp2
+  const size_t wbytes = sizeof(double) * (F * G + H * G + G + H);
+  TS_CUDA(ctx->tmp2.reserve(wbytes));
+  double* dW = ctx->tmp2.as<double>();
+  TS_CUDA(cudaMemcpyAsync(dW, Wx, sizeof(double) * F * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dW + F * G, Wh, sizeof(double) * H * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dW + F * G + H * G, b, sizeof(double) * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dW + F * G + H * G + G, w, sizeof(double) * H, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * B * T * F + 8));
+  TS_CUDA(ctx->out.reserve(sizeof(double) * B));
+  if (T) TS_CUDA(cudaMemcpyAsync(ctx->tmp.p, X, sizeof(double) * B * T * F, cudaMemcpyHostToDevice, ctx->stream));
+  LstmW W;
+  W.Wx = dW;
+  W.Wh = dW + F * G;
+  W.b = dW + F * G + H * G;
+  W.w = dW + F * G + H * G + G;
+  W.H = (int)H;
+  k_lstm_forward_exact<<<(unsigned)((B * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+      W, ctx->tmp.as<double>(), B, (int)T, b_out, ctx->out.as<double>());
+  TS_LAUNCHED();
+  TS_CUDA(cudaMemcpyAsync(raw_out, ctx->out.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
+// Host-side state walk: nests of the scheduled prefix.
+static int host_nests(ts_ctx* ctx, const PipelineDesc& P, const ts_decision* prefix, int64_t n,
+                      std::vector<Nest>& nests) {
+  const int T = P.n_stages;
+  nests.assign(T, Nest());
+  for (int64_t i = 0; i < n; ++i) {
+    const int s = T - 1 - (int)i;
+    const StageDesc& sd = P.st[s];
+    const ts_decision& d = prefix[i];
+    const StageDesc* cs = nullptr;
+    const Nest* cn = nullptr;
+    if (d.anchor >= 0) {
+      if (sd.consumer < 0) return fail(ctx, TS_ERR_ILLEGAL, "compute_at without a sole consumer");
+      cs = &P.st[sd.consumer];
+      cn = &nests[sd.consumer];
+    }
+    const int rc = build_nest(sd, cs, cn, d, nests[s]);
+    if (rc) return fail(ctx, rc, status_name(rc));
+  }
+  return TS_OK;
+}
+
+int ts_candidates(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix,
+                  ts_decision* out, int64_t capacity, int64_t* n_out) {
+  if (!ctx || !n_out || n_prefix < 0) return TS_ERR_ARG;
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  if (n_prefix >= T) return fail(ctx, TS_ERR_ILLEGAL, "state is already complete");
+  std::vector<Nest> nests;
+  int rc = host_nests(ctx, D, prefix, n_prefix, nests);
+  if (rc) return rc;
+  const int s = T - 1 - (int)n_prefix;
+  const StageDesc& sd = D.st[s];
+  const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
+  const Nest* cn = sd.consumer >= 0 ? &nests[sd.consumer] : nullptr;
+  int64_t k = 0;
+  const int64_t cnt = enumerate_candidates(sd, cs, cn, [&](const ts_decision& d) {
+    if (out && k < capacity) out[k] = d;
+    ++k;
+  });
+  if (cnt < 0) return fail(ctx, (int)-cnt, status_name((int)-cnt));
+  *n_out = cnt;
+  if (out && cnt > capacity) return fail(ctx, TS_ERR_ARG, "candidate buffer too small");
+  return TS_OK;
+}
+
+int ts_check_action(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix,
+                    const ts_decision* a) {
+  if (!ctx || !a || n_prefix < 0) return TS_ERR_ARG;
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  if (n_prefix >= T) return fail(ctx, TS_ERR_ILLEGAL, "state is already complete");
+  std::vector<Nest> nests;
+  int rc = host_nests(ctx, D, prefix, n_prefix, nests);
+  if (rc) return rc;
+  const int s = T - 1 - (int)n_prefix;
+  const StageDesc& sd = D.st[s];
+  const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
+  const Nest* cn = sd.consumer >= 0 ? &nests[sd.consumer] : nullptr;
+  const char* why = check_decision(sd, cs, cn, *a);
+  if (why) return fail(ctx, TS_ERR_ILLEGAL, why);
+  return TS_OK;
+}
+
+int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
+              ts_decision* out_decisions, int64_t* visited, double* out_best_v) {
+  if (!ctx || !out_decisions || !visited) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (epsilon > 0.0 && !rng_state) return fail(ctx, TS_ERR_ARG, "noisy evaluation needs an rng");
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  std::vector<Nest> nests(T);
+  std::vector<ts_decision> cands;
+  cands.reserve(1024);
+  // device state rows start as the all-unscheduled normalized matrix
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * T * F));
+  double* state_rows = ctx->tmp.as<double>();
+  TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
+  TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * 4096 + sizeof(Nest)));
+  TS_CUDA(ctx->h_out.reserve(sizeof(double) * 2));
+  uint64_t rng = rng_state ? *rng_state : 0;
+  int64_t vis = 0;
+  double best_v = 0.0;
+  for (int i = 0; i < T; ++i) {
+    const int s = T - 1 - i;
+    const StageDesc& sd = D.st[s];
+    const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
+    const Nest* cn = sd.consumer >= 0 ? &nests[sd.consumer] : nullptr;
+    cands.clear();
+    const int64_t cnt = enumerate_candidates(sd, cs, cn, [&](const ts_decision& d) { cands.push_back(d); });
+    if (cnt <= 0) return fail(ctx, cnt < 0 ? (int)-cnt : TS_ERR_PIPELINE, "candidate enumeration");
+    const int n = (int)cnt;
+    if (n > 4096) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
+    TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * n));
+    TS_CUDA(ctx->rows.reserve(sizeof(double) * F * n));
+    TS_CUDA(ctx->reps.reserve(sizeof(int) * n));
+    TS_CUDA(ctx->raw.reserve(sizeof(double) * n));
+    TS_CUDA(ctx->out.reserve(sizeof(double) * 2));
+    // stage host data in pinned memory: candidate records + consumer nest
+    ts_decision* hs = ctx->h_stage.as<ts_decision>();
+    memcpy(hs, cands.data(), sizeof(ts_decision) * n);
+    Nest* hn = reinterpret_cast<Nest*>(hs + 4096);
+    if (cn) *hn = *cn;
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, hs, sizeof(ts_decision) * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, hn, sizeof(Nest), cudaMemcpyHostToDevice, ctx->stream));
+    k_children_rows<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), s, ctx->records.as<ts_decision>(), n, ctx->nest.as<Nest>(),
+        P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(),
+        ctx->status.as<int>());
+    TS_LAUNCHED();
+    k_dedup<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
+    TS_LAUNCHED();
+    k_children_exact<<<(n * 32 + 127) / 128, 128, 0, ctx->stream>>>(
+        lstm_weights(ctx), P->pre_exact.as<double>(), T, s, ctx->rows.as<double>(), ctx->reps.as<int>(), n,
+        state_rows, ctx->raw.as<double>());
+    TS_LAUNCHED();
+    k_argmin<<<1, 1024, 0, ctx->stream>>>(ctx->raw.as<double>(), ctx->reps.as<int>(), n,
+                                          ctx->target_scale, epsilon, rng, ctx->out.as<double>());
+    TS_LAUNCHED();
+    double* ho = ctx->h_out.as<double>();
+    TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+    int st = 0;
+    TS_CUDA(cudaMemcpy(&st, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (st) {
+      cudaMemset(ctx->status.p, 0, sizeof(int));
+      return fail(ctx, st, std::string("device: ") + status_name(st));
+    }
+    const int best = (int)ho[1];
+    best_v = ho[0];
+    if (best < 0 || best >= n) return fail(ctx, TS_ERR_CUDA, "argmin produced no index");
+    if (epsilon > 0.0) rng += (uint64_t)n * 0x9E3779B97F4A7C15ull;
+    vis += n;
+    out_decisions[i] = cands[best];
+    const int brc = build_nest(sd, cands[best].anchor >= 0 ? cs : nullptr,
+                               cands[best].anchor >= 0 ? cn : nullptr, cands[best], nests[s]);
+    if (brc) return fail(ctx, brc, status_name(brc));
+    TS_CUDA(cudaMemcpyAsync(state_rows + (int64_t)s * F, ctx->rows.as<double>() + (int64_t)best * F,
+                            sizeof(double) * F, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (rng_state && epsilon > 0.0) *rng_state = rng;
+  *visited = vis;
+  if (out_best_v) *out_best_v = best_v;
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
+int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
+                              ts_decision* d_records, int64_t* d_offsets, int64_t* n_records) {
+  if (!ctx || !d_records || !d_offsets || !n_records || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const int T = P->h->n_stages;
+  TS_CUDA(ctx->tmp.reserve(sizeof(ts_decision) * n_states * T + sizeof(int) * n_states + 16));
+  ts_decision* fixed = ctx->tmp.as<ts_decision>();
+  int* depth = reinterpret_cast<int*>(fixed + n_states * T);
+  k_generate<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), seed0, n_states, fixed, depth, ctx->status.as<int>());
+  TS_LAUNCHED();
+  std::vector<int> hd(n_states);
+  std::vector<int64_t> ho(n_states + 1);
+  TS_CUDA(cudaMemcpyAsync(hd.data(), depth, sizeof(int) * n_states, cudaMemcpyDeviceToHost, ctx->stream));
+  int rc = check_device_status(ctx);
+  if (rc) return rc;
+  ho[0] = 0;
+  for (int64_t i = 0; i < n_states; ++i) ho[i + 1] = ho[i] + hd[i];
+  TS_CUDA(cudaMemcpyAsync(d_offsets, ho.data(), sizeof(int64_t) * (n_states + 1), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  k_compact_records<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(fixed, depth, d_offsets,
+                                                                                 n_states, T, d_records);
+  TS_LAUNCHED();
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  *n_records = ho[n_states];
+  return TS_OK;
+}
+
+}  // extern "C"

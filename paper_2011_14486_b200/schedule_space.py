@@ -1,0 +1,354 @@
+"""Host mirror of the reference MDP states/actions (schedule_space.py) and
+the 16-byte decision records the device consumes.
+
+`LayerSchedule` / `ScheduleState` keep the reference's field names and
+rendering, so states built by the reference package itself can be scored
+unchanged (everything below is duck-typed on `.pipeline` / `.decisions`).
+Candidate enumeration and legality run in the native library
+(`ts_candidates`, `ts_check_action`); Python only encodes and decodes.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import IllegalActionError, PipelineError
+from .pipeline_ir import consumers_of, descriptor, schedule_order, topological_order
+
+SPLIT_FACTORS = (8, 32)  # schedule_space.py:28-30
+VEC_WIDTHS = (1, 8)
+MAX_COMPUTE_AT_LEVELS = 3
+FLAG_PARALLEL, FLAG_STORE_AT = 1, 2
+
+
+@dataclass(frozen=True)
+class LayerSchedule:
+    stage: str
+    splits: tuple
+    order: tuple
+    vectorize_width: int = 1
+    parallel: bool = False
+    compute_at: tuple | None = None
+    store_at: tuple | None = None
+
+    def render(self) -> str:
+        splits = ",".join(f"{d}:{f}" for d, f in self.splits) or "-"
+        at = "root" if self.compute_at is None else f"{self.compute_at[0]}@{self.compute_at[1]}"
+        st = "root" if self.store_at is None else f"{self.store_at[0]}@{self.store_at[1]}"
+        return (f"{self.stage} split={splits} order={','.join(self.order)} "
+                f"vec={self.vectorize_width} par={int(self.parallel)} at={at} store={st}")
+
+
+def parse_layer_schedule(text: str) -> LayerSchedule:
+    toks = text.split()
+    if len(toks) != 7:
+        raise PipelineError(f"bad schedule line: {text!r}")
+    kv = {}
+    for tok in toks[1:]:
+        k, eq, v = tok.partition("=")
+        if not eq:
+            raise PipelineError(f"bad schedule token {tok!r}")
+        kv[k] = v
+
+    def site(v):
+        if v == "root":
+            return None
+        c, lvl = v.split("@")
+        return (c, int(lvl))
+
+    try:
+        splits = () if kv["split"] == "-" else tuple(
+            (a, int(b)) for a, b in (x.split(":") for x in kv["split"].split(",")))
+        return LayerSchedule(toks[0], splits, tuple(kv["order"].split(",")), int(kv["vec"]),
+                             bool(int(kv["par"])), site(kv["at"]), site(kv["store"]))
+    except (KeyError, ValueError) as e:
+        raise PipelineError(f"bad schedule line {text!r}: {e}") from None
+
+
+@dataclass(frozen=True)
+class ScheduleState:
+    pipeline: object
+    decisions: tuple = ()
+    _cache: dict = field(default_factory=dict, compare=False, repr=False, hash=False)
+
+    def __hash__(self):
+        return hash((self.pipeline.name, self.decisions))
+
+    @property
+    def scheduled_count(self) -> int:
+        return len(self.decisions)
+
+    @property
+    def order(self):
+        return _info(self.pipeline).sched
+
+    @property
+    def is_complete(self) -> bool:
+        return len(self.decisions) == len(self.pipeline.stages)
+
+    @property
+    def next_stage_name(self) -> str:
+        return self.order[len(self.decisions)]
+
+
+def initial_state(p) -> ScheduleState:
+    if not p.stages:
+        raise PipelineError("pipeline has no stages")
+    return ScheduleState(p)
+
+
+def canonical_key(s) -> str:
+    return s.pipeline.name + "/" + ";".join(d.render() for d in s.decisions)
+
+
+def write_schedule(s) -> str:
+    return "\n".join(d.render() for d in s.decisions) + "\n"
+
+
+# ---------------------------------------------------------------- records
+class _PipelineInfo:
+    """Per-pipeline encoding tables (cached by pipeline object)."""
+
+    def __init__(self, p):
+        self.p = p
+        self.desc = descriptor(p)
+        self.topo = topological_order(p)
+        self.sched = self.topo[::-1]
+        self.T = len(self.topo)
+        by_name = {s.name: s for s in p.stages}
+        self.stages = [by_name[n] for n in self.sched]
+        self.sole = []
+        self.loop_ids = []    # per schedule index: (split-set) -> {loop name: id}
+        for st in self.stages:
+            cons = consumers_of(p, st.name)
+            self.sole.append(cons[0] if len(cons) == 1 else None)
+        self.enc_cache = {}   # id(decision) -> (decision, bytes)
+
+    def loop_table(self, st, split):
+        table = {}
+        for k, (d, _) in enumerate(st.dims):
+            if d in split:
+                table[d + "o"] = 2 * k
+                table[d + "i"] = 2 * k + 1
+            else:
+                table[d] = 2 * k
+        for r, (d, _) in enumerate(st.reduction_dims):
+            table[d] = 8 + r
+        return table
+
+    def encode(self, idx: int, d) -> bytes:
+        hit = self.enc_cache.get(id(d))
+        if hit is not None and hit[0] is d:
+            return hit[1]
+        st = self.stages[idx]
+        if d.stage != st.name:
+            raise IllegalActionError(
+                f"expected a decision for stage {st.name!r}, got {d.stage!r}")
+        rec = np.zeros(1, _lib.DECISION_DTYPE)[0]
+        pure = [n for n, _ in st.dims]
+        split = {}
+        for dim, f in d.splits:
+            if dim in split:
+                raise IllegalActionError(f"{st.name}: dim {dim} split twice")
+            if dim not in pure:
+                raise IllegalActionError(f"{st.name}: cannot split non-pure dim {dim}")
+            if f < 2:
+                raise IllegalActionError(f"{st.name}: split factor {f} < 2")
+            if f > 255:
+                raise PipelineError(f"{st.name}: split factor {f} outside the record envelope")
+            split[dim] = f
+            rec["split"][pure.index(dim)] = f
+        table = self.loop_table(st, split)
+        if sorted(d.order) != sorted(table) or len(d.order) > 8:
+            raise IllegalActionError(
+                f"{st.name}: order {d.order} is not a permutation of loops {sorted(table)}")
+        rec["order"][:] = 0xFF
+        for j, name in enumerate(d.order):
+            rec["order"][j] = table[name]
+        rec["n_loops"] = len(d.order)
+        if not 1 <= d.vectorize_width <= 255:
+            raise IllegalActionError(f"{st.name}: bad vectorize width {d.vectorize_width}")
+        rec["vec"] = d.vectorize_width
+        flags = FLAG_PARALLEL if d.parallel else 0
+        if d.compute_at is None:
+            rec["anchor"] = -1
+            if d.store_at is not None:
+                raise IllegalActionError(f"{st.name}: store_at must be Root or the compute_at site")
+        else:
+            cname, lvl = d.compute_at
+            if self.sole[idx] != cname:
+                cons = list(consumers_of(self.p, st.name))
+                raise IllegalActionError(
+                    f"{st.name}: compute_at target must be the sole consumer (consumers: {cons})")
+            if not 0 <= lvl < 8:
+                raise IllegalActionError(f"{st.name}: loop level {lvl} does not exist in {cname}'s nest")
+            rec["anchor"] = lvl
+            if d.store_at is not None:
+                if d.store_at != d.compute_at:
+                    raise IllegalActionError(
+                        f"{st.name}: store_at must be Root or the compute_at site")
+                flags |= FLAG_STORE_AT
+        rec["flags"] = flags
+        b = rec.tobytes()
+        self.enc_cache[id(d)] = (d, b)
+        return b
+
+    def decode(self, idx: int, rec) -> LayerSchedule:
+        st = self.stages[idx]
+        split = {}
+        splits = []
+        for k, (dname, _) in enumerate(st.dims):
+            f = int(rec["split"][k])
+            if f:
+                split[dname] = f
+                splits.append((dname, f))
+        inv = {v: k for k, v in self.loop_table(st, split).items()}
+        order = tuple(inv[int(x)] for x in rec["order"][: int(rec["n_loops"])])
+        anchor = int(rec["anchor"])
+        at = None if anchor < 0 else (self.sole[idx], anchor)
+        store = at if (int(rec["flags"]) & FLAG_STORE_AT) else None
+        return LayerSchedule(st.name, tuple(splits), order, int(rec["vec"]),
+                             bool(int(rec["flags"]) & FLAG_PARALLEL), at, store)
+
+    def records_of(self, s) -> bytes:
+        cached = getattr(s, "_cache", None)
+        if isinstance(cached, dict):
+            hit = cached.get("ts_records")
+            if hit is not None:
+                return hit
+        out = b"".join(self.encode(i, d) for i, d in enumerate(s.decisions))
+        if isinstance(cached, dict):
+            cached["ts_records"] = out
+        return out
+
+
+_INFO: dict = {}
+
+
+def _info(p) -> _PipelineInfo:
+    inf = _INFO.get(p)
+    if inf is None:
+        inf = _INFO[p] = _PipelineInfo(p)
+    return inf
+
+
+def encode_states(states):
+    """Group states by pipeline -> [(pipeline_info, indices, records, offsets)]."""
+    groups = {}
+    for i, s in enumerate(states):
+        groups.setdefault(s.pipeline, []).append(i)
+    out = []
+    for p, idxs in groups.items():
+        inf = _info(p)
+        chunks = [inf.records_of(states[i]) for i in idxs]
+        lens = np.fromiter((len(c) // 16 for c in chunks), dtype=np.int64, count=len(chunks))
+        if np.any(lens > inf.T):
+            raise IllegalActionError("state has more decisions than stages")
+        offsets = np.zeros(len(chunks) + 1, dtype=np.int64)
+        np.cumsum(lens, out=offsets[1:])
+        recs = np.frombuffer(b"".join(chunks), dtype=_lib.DECISION_DTYPE)
+        out.append((inf, idxs, recs, offsets))
+    return out
+
+
+def _host_ctx():
+    """Context for host-side library calls (enumeration/legality): the device
+    context when a GPU is present, else a host-only context."""
+    return _lib.host_context()
+
+
+def candidate_actions(s):
+    """All legal decisions for the next stage, in the reference's order
+    (schedule_space.py:379-452), enumerated by the native library."""
+    if s.is_complete:
+        raise IllegalActionError("state is already complete")
+    inf = _info(s.pipeline)
+    ctx = _host_ctx()
+    pid = ctx.pipeline_id(inf.desc)
+    prefix = np.frombuffer(inf.records_of(s), dtype=_lib.DECISION_DTYPE)
+    cap = 4096
+    buf = np.zeros(cap, dtype=_lib.DECISION_DTYPE)
+    n = ctypes.c_int64()
+    ctx.check(ctx.lib.ts_candidates(ctx.h, pid, _lib._p(prefix) if len(prefix) else None,
+                                    len(prefix), _lib._p(buf), cap, ctypes.byref(n)))
+    idx = len(s.decisions)
+    out = []
+    for r in buf[: n.value]:
+        d = inf.decode(idx, r)
+        inf.enc_cache[id(d)] = (d, r.tobytes())
+        out.append(d)
+    return out
+
+
+def check_action(s, a) -> str | None:
+    """None if legal, else the violated invariant (schedule_space.py:288-347)."""
+    if s.is_complete:
+        return "state is already complete"
+    if a.stage != s.next_stage_name:
+        return f"expected a decision for stage {s.next_stage_name!r}, got {a.stage!r}"
+    inf = _info(s.pipeline)
+    try:
+        rec = np.frombuffer(inf.encode(len(s.decisions), a), dtype=_lib.DECISION_DTYPE)
+    except IllegalActionError as e:
+        return str(e)
+    ctx = _host_ctx()
+    pid = ctx.pipeline_id(inf.desc)
+    prefix = np.frombuffer(inf.records_of(s), dtype=_lib.DECISION_DTYPE)
+    rc = ctx.lib.ts_check_action(ctx.h, pid, _lib._p(prefix) if len(prefix) else None,
+                                 len(prefix), _lib._p(rec))
+    if rc == _lib.TS_OK:
+        return None
+    if rc == _lib.TS_ERR_ILLEGAL:
+        return ctx.lib.ts_last_error(ctx.h).decode()
+    ctx.check(rc)
+    return None
+
+
+def apply(s, a):
+    """Extend a state by one decision (schedule_space.py:350-358)."""
+    reason = check_action(s, a)
+    if reason is not None:
+        raise IllegalActionError(reason)
+    inf = _info(s.pipeline)
+    child = ScheduleState(s.pipeline, tuple(s.decisions) + (a,))
+    child._cache["ts_records"] = inf.records_of(s) + inf.encode(len(s.decisions), a)
+    return child
+
+
+def child_state(s, a):
+    """`apply` without the legality round trip, for actions that came out of
+    candidate_actions(s)."""
+    inf = _info(s.pipeline)
+    child = ScheduleState(s.pipeline, tuple(s.decisions) + (a,))
+    child._cache["ts_records"] = inf.records_of(s) + inf.encode(len(s.decisions), a)
+    return child
+
+
+def state_from_decisions(p, decisions):
+    s = initial_state(p)
+    for d in decisions:
+        s = apply(s, d)
+    return s
+
+
+def read_schedule(p, text: str):
+    decisions = [parse_layer_schedule(line) for line in text.splitlines()
+                 if line.strip() and not line.lstrip().startswith("#")]
+    return state_from_decisions(p, decisions)
+
+
+def state_from_key(p, key: str):
+    prefix = p.name + "/"
+    if not key.startswith(prefix):
+        raise PipelineError(f"key {key!r} does not belong to pipeline {p.name!r}")
+    body = key[len(prefix):]
+    return state_from_decisions(p, [parse_layer_schedule(t) for t in body.split(";") if t])
+
+
+def default_action(s) -> LayerSchedule:
+    st = s.pipeline.stage(s.next_stage_name)
+    return LayerSchedule(st.name, (), tuple(d for d, _ in st.all_dims))

@@ -1,0 +1,73 @@
+// TEST INFRASTRUCTURE ONLY: host build of ts_core.cuh (the integer nest math,
+// u256, correctly rounded conversions and the glibc-log2 port shared with the
+// sm_100a kernels) so the CPU suite can check it against the reference's
+// golden feature matrices without a GPU.  Never linked into the product.
+#include <cstring>
+#include <vector>
+
+#include "../../paper_2011_14486_b200/csrc/ts_core.cuh"
+
+using namespace ts;
+
+extern "C" int core_featurize(const int64_t* desc, int64_t n_words, const ts_decision* rec,
+                              const int64_t* offsets, int64_t n, double* out) {
+  static PipelineDesc P;
+  memset(&P, 0, sizeof P);
+  const int T = (int)desc[1];
+  P.n_stages = T;
+  P.n_slots = (int)desc[2];
+  for (int s = 0; s < T; ++s) {
+    const int64_t* w = desc + 4 + 48 * s;
+    StageDesc& sd = P.st[s];
+    sd.n_pure = (int)w[0];
+    sd.n_red = (int)w[1];
+    for (int k = 0; k < 8; ++k) sd.ext[k] = w[2 + k];
+    sd.pure_points = w[10]; sd.red_points = w[11]; sd.domain_points = w[12];
+    sd.i_points = w[13]; sd.i_flops = w[14]; sd.i_in_bytes = w[15]; sd.i_out_bytes = w[16];
+    sd.n_inputs = (int)w[17]; sd.ov_window = (int)w[18]; sd.ov_stride = (int)w[19];
+    sd.consumer = (int)w[20]; sd.n_cedges = (int)w[21];
+    for (int e = 0; e < 2; ++e)
+      for (int k = 0; k < 4; ++k) {
+        sd.cdim[e][k] = (int)w[22 + 4 * e + k];
+        sd.cstride[e][k] = w[30 + 4 * e + k];
+        sd.cwindow[e][k] = w[38 + 4 * e + k];
+      }
+    sd.slot = (int)w[46];
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double* o = out + i * T * 16;
+    for (int s = 0; s < T; ++s) {
+      intrinsic_features(P.st[s], o + s * 16);
+      for (int k = 8; k < 16; ++k) o[s * 16 + k] = 0.0;
+    }
+    std::vector<Nest> slots(16);
+    const int d = (int)(offsets[i + 1] - offsets[i]);
+    for (int j = 0; j < d; ++j) {
+      const int s = T - 1 - j;
+      const StageDesc& sd = P.st[s];
+      const ts_decision& dec = rec[offsets[i] + j];
+      const StageDesc* cs = dec.anchor >= 0 ? &P.st[sd.consumer] : nullptr;
+      const Nest* cn = dec.anchor >= 0 ? &slots[cs->slot] : nullptr;
+      Nest nn;
+      int rc = build_nest(sd, cs, cn, dec, nn);
+      if (!rc) rc = acquired_features(sd, nn, dec, o + s * 16 + 8);
+      if (rc) return rc;
+      if (sd.slot >= 0) slots[sd.slot] = nn;
+    }
+  }
+  return 0;
+}
+
+extern "C" double core_log2(double x) { return glibc_log2(x); }
+
+extern "C" double core_div(const uint64_t* n4, uint64_t d) {
+  u256 a;
+  for (int i = 0; i < 4; ++i) a.w[i] = n4[i];
+  return u256_div_u64_to_double(a, d);
+}
+
+extern "C" double core_to_double(const uint64_t* n4) {
+  u256 a;
+  for (int i = 0; i < 4; ++i) a.w[i] = n4[i];
+  return u256_to_double(a);
+}

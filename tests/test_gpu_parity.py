@@ -1,0 +1,132 @@
+"""Parity of the sm_100a path against the reference's golden vectors and the
+CPU oracle.  Every call goes through the C-ABI library (libtensched_b200.so).
+
+Tolerances: features are bit-exact; V in EXACT mode (fp64, Cython op order,
+CUDA exp/tanh instead of glibc's) within 1e-12 relative; V in FAST mode
+(tensor cores) within 1e-4 relative (BASELINE.json north_star, fp32 leg);
+greedy schedules and visited counts identical."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import bits, oracle_decisions, oracle_params, pipeline_from, product_states
+from paper_2011_14486_b200 import _lib
+from paper_2011_14486_b200 import schedule_space as ss
+from paper_2011_14486_b200.featurizer import featurize_states
+from paper_2011_14486_b200.search import (NoiseConfig, SearchRng, greedy_schedule,
+                                          greedy_schedule_gpu, model_value)
+from paper_2011_14486_b200.value_model import MODE_EXACT, MODE_FAST, load, predict_states
+
+pytestmark = pytest.mark.gpu
+
+EXACT_RTOL = 1e-12
+FAST_RTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def v0(v0_path):
+    return load(v0_path)
+
+
+def test_features_bit_exact(state_sets, gpu_ctx):
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        got = np.stack(featurize_states(product_states(p, z["keys"])))
+        assert np.array_equal(bits(got), bits(z["features"])), name
+
+
+def test_values_exact(state_sets, v0):
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        got = predict_states(v0, product_states(p, z["keys"]), mode=MODE_EXACT)
+        np.testing.assert_allclose(got, z["values"], rtol=EXACT_RTOL, atol=0, err_msg=name)
+
+
+def test_lstm_forward_exact(golden, v0):
+    from paper_2011_14486_b200.backend import lstm_forward
+    z = np.load(golden / "lstm_forward.npz")
+    raw = lstm_forward(z["X"], v0.Wx, v0.Wh, v0.b, v0.w, v0.b_out)
+    np.testing.assert_allclose(raw, z["raw"], rtol=EXACT_RTOL, atol=1e-13)
+
+
+def test_position_and_batch_independence(state_sets, v0):
+    z = state_sets["vgg16"]
+    p = pipeline_from(z)
+    states = product_states(p, z["keys"])
+    one = np.array([predict_states(v0, [s])[0] for s in states[:6]])
+    mixed = states[::-1] + states[:6]
+    many = predict_states(v0, mixed)
+    assert np.array_equal(bits(many[-6:]), bits(one))
+    assert np.array_equal(bits(many[: len(states)][::-1][:6]), bits(one))
+
+
+def test_greedy_fused_matches_reference(greedy_golden, v0):
+    for key, g in greedy_golden.items():
+        p = pipeline_from(g)
+        s, visited, v = greedy_schedule_gpu(p, v0, return_value=True)
+        assert [d.render() for d in s.decisions] == g["schedule"], key
+        assert visited == g["visited"], key
+        assert abs(v / float.fromhex(g["predicted"]) - 1) < EXACT_RTOL, key
+
+
+def test_greedy_generic_v_callable(greedy_golden, v0):
+    for key in ("ref:pipelines/toys/t3_chain.pl", "ref:pipelines/deep/p12_deep.pl",
+                "assets/pipelines/nets/crp2d.pl"):
+        g = greedy_golden[key]
+        s, visited = greedy_schedule(pipeline_from(g), model_value(v0))
+        assert [d.render() for d in s.decisions] == g["schedule"], key
+        assert visited == g["visited"]
+
+
+def test_noisy_greedy(noisy_golden, greedy_golden, v0):
+    for key, g in noisy_golden.items():
+        base, seed = key.split("#")
+        p = pipeline_from(greedy_golden[base])
+        rng = SearchRng(int(seed))
+        s, visited = greedy_schedule_gpu(p, v0, NoiseConfig(0.25), rng)
+        assert [d.render() for d in s.decisions] == g["schedule"], key
+        assert visited == g["visited"] and rng.state == g["rng_state"], key
+
+
+def test_device_generator_matches_oracle_walk(state_sets, gpu_ctx):
+    import ctypes
+    import torch
+    for name in ("t3_chain", "p12_deep", "vgg16", "resnet18"):
+        z = state_sets[name]
+        p = pipeline_from(z)
+        inf = ss._info(p)
+        pid = gpu_ctx.pipeline_id(inf.desc)
+        n = len(z["seeds"])
+        recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
+        offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        nrec = ctypes.c_int64()
+        gpu_ctx.check(gpu_ctx.lib.ts_generate_states_device(
+            gpu_ctx.h, pid, int(z["seeds"][0]), n, recs.data_ptr(), offs.data_ptr(),
+            ctypes.byref(nrec)))
+        hr = np.frombuffer(recs[: nrec.value * 16].cpu().numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
+        ho = offs.cpu().numpy()
+        for i in range(n):
+            dec = [inf.decode(k, r).render() for k, r in enumerate(hr[ho[i]:ho[i + 1]])]
+            assert p.name + "/" + ";".join(dec) == str(z["keys"][i]), (name, i)
+
+
+def test_fast_mode_within_tolerance(state_sets, v0):
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        states = product_states(p, z["keys"])
+        fast = predict_states(v0, states, mode=MODE_FAST)
+        np.testing.assert_allclose(fast, z["values"], rtol=FAST_RTOL, atol=0, err_msg=name)
+
+
+def test_oracle_agrees_on_fresh_states(v0_path, v0, greedy_golden):
+    params = oracle_params(v0_path)
+    p = pipeline_from(greedy_golden["assets/pipelines/nets/vgg16.pl"])
+    P = O.Pipe(p)
+    decs = [O.random_partial(P, seed) for seed in range(1000, 1024)]
+    want = O.values(params, P, decs)
+    states = [ss.state_from_decisions(p, d) for d in decs]
+    np.testing.assert_allclose(predict_states(v0, states), want, rtol=EXACT_RTOL)
+    feats = np.stack(featurize_states(states))
+    for i, d in enumerate(decs):
+        assert np.array_equal(bits(feats[i]), bits(O.features(P, d)))

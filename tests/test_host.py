@@ -1,0 +1,142 @@
+"""Host-side logic of the product (no GPU): the C-ABI library loads and
+exports every declared symbol, the host mirror parses/encodes like the
+reference, native candidate enumeration and legality match the golden
+vectors, and the shared nest/feature core (csrc/ts_core.cuh, host build)
+reproduces the reference's feature matrices bit for bit."""
+
+import ctypes
+import math
+import pathlib
+import random
+import re
+
+import numpy as np
+import pytest
+
+from helpers import bits, pipeline_from, product_states
+from paper_2011_14486_b200 import _lib
+from paper_2011_14486_b200 import pipeline_ir as pi
+from paper_2011_14486_b200 import schedule_space as ss
+from paper_2011_14486_b200.errors import IllegalActionError, ParseError
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load_library()
+    header = (ROOT / "include" / "tensched_b200.h").read_text()
+    names = re.findall(r"^\s*(?:int|void|const char\*|int64_t|void\*)\s+\**(ts_\w+)\(", header, re.M)
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lib.ts_abi_version() == 1
+
+
+def test_host_only_context_refuses_device_work():
+    ctx = _lib.Context(-1)
+    out = np.zeros(1)
+    rc = ctx.lib.ts_score_states(ctx.h, 0, None, _lib._p(np.zeros(2, np.int64)), 1, 0, _lib._p(out))
+    assert rc != 0
+
+
+def test_parse_and_topo_match_reference(greedy_golden):
+    import oracle as O
+    for key, g in greedy_golden.items():
+        p = pipeline_from(g)
+        assert p.name == g["pipeline"]
+        assert pi.topological_order(p) == O.Pipe(p).topo
+
+
+def test_parse_errors():
+    with pytest.raises(ParseError):
+        pi.parse_pipeline("pipeline x\nstage a dims x:4 flops 1\n  in z map x*1+1\n")
+    with pytest.raises(ParseError):
+        pi.parse_pipeline("stage a dims x:4 flops 1\n")
+
+
+def test_candidates_match_golden(candidates_golden, greedy_golden):
+    for key, walk in candidates_golden.items():
+        p = pipeline_from(greedy_golden[key])
+        rng = random.Random(0)
+        s = ss.initial_state(p)
+        r5 = __import__("oracle").SplitMix(5)
+        for step in walk:
+            c = ss.candidate_actions(s)
+            assert [a.render() for a in c] == step, (key, len(s.decisions))
+            s = ss.apply(s, c[r5.randrange(len(c))])
+
+
+def test_encode_decode_roundtrip(state_sets):
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        states = product_states(p, z["keys"][:6])
+        for inf, idxs, recs, offs in ss.encode_states(states):
+            for j, i in enumerate(idxs):
+                dec = [inf.decode(k, r) for k, r in enumerate(recs[offs[j]:offs[j + 1]])]
+                assert [d.render() for d in dec] == [d.render() for d in states[i].decisions]
+
+
+def test_check_action_rejects_illegal(greedy_golden):
+    p = pipeline_from(greedy_golden["ref:pipelines/toys/t2_stencil.pl"])
+    s = ss.initial_state(p)
+    blur = ss.LayerSchedule("blur", (("x", 8),), ("xo", "xi"), 1, False, None, None)
+    s = ss.apply(s, blur)
+    bad = [
+        ss.LayerSchedule("pre", (("x", 7),), ("xo", "xi")),             # does not divide 66
+        ss.LayerSchedule("pre", (), ("x",), 3),                          # bad width
+        ss.LayerSchedule("pre", (), ("x",), 1, False, ("blur", 5)),      # no such level
+        ss.LayerSchedule("pre", (), ("x",), 1, False, None, ("blur", 0)),  # store without compute
+        ss.LayerSchedule("blur", (), ("x",)),                            # wrong stage
+    ]
+    for a in bad:
+        assert ss.check_action(s, a) is not None, a
+        with pytest.raises(IllegalActionError):
+            ss.apply(s, a)
+    ok = ss.LayerSchedule("pre", (), ("x",), 1, False, ("blur", 0), ("blur", 0))
+    assert ss.check_action(s, ok) is None
+
+
+def test_descriptor_envelope(greedy_golden):
+    for g in greedy_golden.values():
+        d = pi.descriptor(pipeline_from(g))
+        assert d[0] == pi.DESC_MAGIC and d.size == 4 + d[1] * pi.DESC_STAGE_WORDS
+        assert 0 <= d[2] <= 16
+
+
+def test_native_core_log2_matches_libm(native_core):
+    for i in range(1, 1 << 17):
+        assert native_core.core_log2(float(i)) == math.log2(i)
+    rng = random.Random(7)
+    for _ in range(20000):
+        x = rng.random() * 2.0 ** rng.randint(-40, 80)
+        if x > 0:
+            assert native_core.core_log2(x) == math.log2(x)
+
+
+def test_native_core_bigint_rounding(native_core):
+    rng = random.Random(3)
+
+    def limbs(n):
+        return np.array([(n >> (64 * k)) & ((1 << 64) - 1) for k in range(4)], dtype=np.uint64)
+
+    for _ in range(20000):
+        n = rng.getrandbits(rng.randint(1, 200)) + 1
+        d = rng.getrandbits(rng.randint(1, 63)) + 1
+        a = limbs(n)
+        assert native_core.core_div(a.ctypes.data, d) == n / d
+        assert native_core.core_to_double(a.ctypes.data) == float(n)
+        tie = ((rng.getrandbits(52) | (1 << 52)) * 2 + 1) << rng.randint(0, 150)
+        assert native_core.core_to_double(limbs(tie).ctypes.data) == float(tie)
+
+
+def test_native_core_features_bit_exact(state_sets, native_core):
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        states = product_states(p, z["keys"])
+        for inf, idxs, recs, offs in ss.encode_states(states):
+            out = np.empty((len(idxs), inf.T, 16))
+            rc = native_core.core_featurize(inf.desc.ctypes.data, inf.desc.size,
+                                            recs.ctypes.data, offs.ctypes.data, len(idxs),
+                                            out.ctypes.data)
+            assert rc == 0
+            assert np.array_equal(bits(out), bits(z["features"][idxs])), name
