@@ -1,0 +1,371 @@
+"""Benchmark: candidate schedules scored per second (BASELINE.json metric) on
+the synthetic scoring sweep - random partial schedules over VGG-16 (T=34),
+scored with the v0 value function - plus the fused greedy wall times.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--states M] [--mode fast|exact]
+
+One process per GPU (torchrun for N>1, NCCL only for the barrier and the
+max-over-ranks reduction of the timings - scoring shards with no data-path
+collective).  A step scores M states per GPU (default 2^20); states are
+generated on the device by the reference's own random walk (SearchRng per
+state, untimed) and stay resident in HBM; records (~280 MB per GPU) exceed
+the 126 MB L2, so no explicit flush is needed between steps.
+
+`value`  = states scored per second over all ranks, device-resident inputs.
+`e2e`    = the same through the C-ABI with HOST buffers (ts_score_states):
+           H2D of the records/offsets and D2H of V inside the timed region.
+`cpu_baseline` = the unmodified reference (oracle/_ref, tensched with its
+           Cython kernel) on this host: predict_states on fresh VGG-16 states,
+           one process and a pool of all cores.
+`--impl reference` times that reference alone (rank 0) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import pathlib
+import subprocess
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GOLD = ROOT / "tests" / "golden"
+VGG = ROOT / "assets" / "pipelines" / "nets" / "vgg16.pl"
+FLOPS_PER_STEP = 12352  # 2*48*128 MMA + 64 readout flops per state-timestep
+RECORD_BYTES = 16
+ROW_BYTES = 128
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--states", type=int, default=1 << 20, help="states per GPU per step")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--cpu-states", type=int, default=1500, help="reference states per process")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-greedy", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index):
+        self.proc = None
+        self.path = pathlib.Path(f"/tmp/ts_clocks_{os.getpid()}.csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        sm = sorted(r[0] for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- reference (CPU)
+def _ref_import():
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "tensched").exists():
+        raise RuntimeError("oracle/_ref is not built (run oracle/build_ref.sh here)")
+    sys.path.insert(0, str(ref))
+    import tensched  # noqa: F401
+    from tensched import backend
+    assert backend.BACKEND == "cython"
+    return ref
+
+
+def _ref_worker(args):
+    """Generate n fresh states with the reference's own walk (untimed), then
+    time the reference's predict_states on them (features not cached)."""
+    seed0, n, ckpt = args
+    _ref_import()
+    from tensched.pipeline_ir import parse_pipeline
+    from tensched.schedule_space import apply, candidate_actions, initial_state
+    from tensched.search import SearchRng
+    from tensched.value_model import load, predict_states
+    params = load(ckpt)
+    p = parse_pipeline(VGG.read_text())
+    states = []
+    for seed in range(seed0, seed0 + n):
+        rng = SearchRng(seed)
+        d = rng.randrange(len(p.stages)) + 1
+        s = initial_state(p)
+        for _ in range(d):
+            c = candidate_actions(s)
+            s = apply(s, c[rng.randrange(len(c))])
+        states.append(s)
+    t0 = time.perf_counter()
+    predict_states(params, states, jobs=1)
+    return time.perf_counter() - t0, len(states)
+
+
+def cpu_reference(per_proc: int, seed0: int = 1, single: bool = True):
+    """The reference's own predict_states on fresh VGG-16 sweep states: one
+    process, then a pool of os.cpu_count() processes over disjoint shards."""
+    import multiprocessing as mp
+    _ref_import()
+    ckpt = str(GOLD / "v0.ckpt")
+    out = {}
+    if single:
+        dt, n = _ref_worker((seed0, per_proc, ckpt))
+        out["single"], out["single_sample"] = n / dt, n
+    cores = os.cpu_count() or 1
+    shards = [(seed0 + i * per_proc, per_proc, ckpt) for i in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_ref_worker, shards)
+    out["pool"] = sum(r[1] for r in res) / max(r[0] for r in res)
+    out["pool_sample"] = per_proc * cores
+    out["cores"] = cores
+    return out
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    rates = []
+    for step in range(args.warmup + args.steps):
+        r = cpu_reference(800, seed0=1 + step * 100003, single=False)
+        if step >= args.warmup:
+            rates.append(r["pool"])
+    v = sum(rates) / len(rates)
+    line = {
+        "metric": "candidate schedules scored/sec", "value": v, "unit": "states/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "vgg16 synthetic scoring sweep (random partial schedules, "
+                               "SearchRng walk, v0.ckpt)", "pipeline": "vgg16", "T": 34},
+        "cpu_baseline": {"value": v, "unit": "states/s", "cores": cores, "kind": "reference",
+                         "sample": "tensched.predict_states (Cython backend) on fresh VGG-16 "
+                                   "states, a pool of os.cpu_count() processes per step"},
+        "e2e": {"value": v, "unit": "states/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2011_14486_b200 import _lib
+    from paper_2011_14486_b200.pipeline_ir import parse_pipeline
+    from paper_2011_14486_b200.schedule_space import _info
+    from paper_2011_14486_b200.value_model import load
+
+    ctx = _lib.context(local)
+    params = load(GOLD / "v0.ckpt")
+    ctx.set_params(params)
+    p = parse_pipeline(VGG.read_text())
+    inf = _info(p)
+    pid = ctx.pipeline_id(inf.desc)
+    T = inf.T
+    M = args.states
+    mode = _lib.MODE_FAST if args.mode == "fast" else _lib.MODE_EXACT
+    dev = torch.device("cuda", local)
+
+    # ---- untimed: generate this rank's shard of states on the device
+    seed0 = 1 + rank * M
+    recs = torch.empty(M * T * 16, dtype=torch.uint8, device=dev)
+    offs = torch.empty(M + 1, dtype=torch.int64, device=dev)
+    nrec = ctypes.c_int64()
+    ctx.check(ctx.lib.ts_generate_states_device(ctx.h, pid, seed0, M, recs.data_ptr(),
+                                                offs.data_ptr(), ctypes.byref(nrec)))
+    n_records = nrec.value
+    out = torch.empty(M, dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.lib.ts_stream(ctx.h), device=dev)
+
+    def step():
+        ctx.check(ctx.lib.ts_score_states_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M,
+                                                 n_records, mode, out.data_ptr()))
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    vals = out.cpu().numpy()
+    assert np.all(np.isfinite(vals)) and np.all(vals > 0), "non-positive V"
+
+    # ---- device-resident timed region
+    times = np.zeros(4)
+    counts = np.zeros(4, dtype=np.int64)
+    ctx.lib.ts_kernel_times(ctx.h, _lib._p(times), _lib._p(counts), 1)
+    ctx.lib.ts_set_timing(ctx.h, 1)
+    launches0 = ctx.launches()
+    clocks = ClockSampler(local)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ctx.lib.ts_set_timing(ctx.h, 0)
+    ctx.lib.ts_kernel_times(ctx.h, _lib._p(times), _lib._p(counts), 1)
+    launches = ctx.launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_states = M * world * args.steps
+    value = total_states / (ms_max / 1e3)
+
+    # ---- e2e: host buffers through the C-ABI (pinned), H2D + D2H inside
+    h_recs = torch.empty(n_records * 16, dtype=torch.uint8, pin_memory=True)
+    h_recs.copy_(recs[: n_records * 16])
+    h_offs = torch.empty(M + 1, dtype=torch.int64, pin_memory=True)
+    h_offs.copy_(offs)
+    h_out = torch.empty(M, dtype=torch.float64, pin_memory=True)
+
+    def e2e_step():
+        ctx.check(ctx.lib.ts_score_states(ctx.h, pid, h_recs.data_ptr(), h_offs.data_ptr(), M,
+                                          mode, h_out.data_ptr()))
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    ev3.record(stream)
+    barrier()
+    t2 = torch.tensor([ev2.elapsed_time(ev3)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_value = total_states / (float(t2.item()) / 1e3)
+    assert np.allclose(h_out.numpy(), out.cpu().numpy(), rtol=0, atol=0)
+
+    # ---- roofline of the dominant kernel
+    offs_h = h_offs.numpy()
+    depths = np.diff(offs_h)
+    timesteps = int(depths.sum())
+    names = ["featurize", "lstm_exact", "lstm_fast", "other"]
+    avg = {names[k]: times[k] / counts[k] for k in range(4) if counts[k]}
+    dom = max(avg, key=lambda k: times[names.index(k)])
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    if dom == "featurize":
+        bytes_per_launch = n_records * (RECORD_BYTES + ROW_BYTES) + 8 * (M + 1)
+        achieved = bytes_per_launch / (avg[dom] / 1e3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"kernel": "k_featurize_rows", "bound": "hbm", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "algorithmic": "16 B record read + 128 B row written per scheduled stage"}
+    else:
+        flops_per_launch = FLOPS_PER_STEP * timesteps
+        achieved = flops_per_launch / (avg[dom] / 1e3) / 1e12
+        peak = peaks.get("bf16_tflops", 1590.0)
+        roof = {"kernel": "k_lstm_tc" if dom == "lstm_fast" else "k_score_exact", "bound": "tensor",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None,
+                "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
+    roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
+
+    greedy = {}
+    if rank == 0 and not args.no_greedy:
+        from paper_2011_14486_b200.search import greedy_schedule_gpu
+        for net in ("resnet18", "resnet50", "mobilenet_v2"):
+            pn = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
+            greedy_schedule_gpu(pn, params)  # warm (descriptor upload, prefix)
+            t0 = time.perf_counter()
+            s, visited = greedy_schedule_gpu(pn, params)
+            greedy[net] = {"wall_s": round(time.perf_counter() - t0, 4), "visited": visited}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            r = cpu_reference(args.cpu_states)
+            cpu = {"value": r["pool"], "unit": "states/s", "cores": r["cores"], "kind": "reference",
+                   "single_process": r["single"],
+                   "sample": f"tensched predict_states (Cython) on fresh VGG-16 sweep states: "
+                             f"{r['single_sample']} states in 1 process, {r['pool_sample']} over "
+                             f"{r['cores']} processes"}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "states/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "candidate schedules scored/sec", "value": value, "unit": "states/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if mode == _lib.MODE_FAST else "f64",
+            "data": "synthetic",
+            "config": {"workload": "vgg16 synthetic scoring sweep: random partial schedules "
+                                   "(SearchRng walk), v0.ckpt", "pipeline": "vgg16", "T": T,
+                       "states_per_gpu": M, "mean_depth": float(depths.mean()),
+                       "mode": args.mode, "l2": "inputs larger than L2 (records "
+                       f"{n_records * 16 / 1e6:.0f} MB/GPU)", "parallelism": f"shard{world}"},
+            "e2e": {"value": e2e_value, "unit": "states/s",
+                    "h2d_bytes_per_step": int(n_records * 16 + 8 * (M + 1)),
+                    "d2h_bytes_per_step": int(8 * M)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "greedy_wall_s": greedy,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

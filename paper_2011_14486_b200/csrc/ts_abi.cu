@@ -508,17 +508,21 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
   const int T = P->h->n_stages;
   if (mode == TS_MODE_EXACT) {
     TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1)));
-    KTimer kt0(ctx, TS_K_FEATURIZE);
-    k_featurize_rows<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
-        P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
-        ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
-    TS_LAUNCHED();
-    const int64_t threads = n_states * 32;
-    KTimer kt1(ctx, TS_K_LSTM_EXACT);
-    k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
-        lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
-        ctx->target_scale, d_out);
-    TS_LAUNCHED();
+    {
+      KTimer kt(ctx, TS_K_FEATURIZE);
+      k_featurize_rows<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
+      TS_LAUNCHED();
+    }
+    {
+      const int64_t threads = n_states * 32;
+      KTimer kt(ctx, TS_K_LSTM_EXACT);
+      k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
+          lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
+          ctx->target_scale, d_out);
+      TS_LAUNCHED();
+    }
     return TS_OK;
   }
   if (mode == TS_MODE_FAST) {
