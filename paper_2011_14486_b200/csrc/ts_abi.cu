@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <string>
 #include <vector>
@@ -98,6 +99,8 @@ struct ts_ctx {
   DevBuf status, records, offsets, rows, out, reps, raw, nest, tmp, tmp2;
   HostBuf h_stage, h_out;
   int64_t launches = 0;
+  int sm_count = 148;
+  bool tc_attr_set = false;
   // optional per-kernel-class timing (bench.py): events around launches on
   // the context stream, resolved at the next host synchronization
   bool timing = false;
@@ -311,6 +314,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
     return TS_ERR_NO_DEVICE;
   auto* ctx = new ts_ctx();
   ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess)
@@ -465,8 +469,13 @@ int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh
   ctx->b_out = b_out;
   ctx->target_scale = target_scale;
   ++ctx->params_version;
-  const int rc = tc_pack_weights(ctx->stream, Wx, Wh, b, w, hidden, &ctx->fast_w.p, &ctx->fast_w.bytes);
-  if (rc) return fail(ctx, rc, "packing tensor-core weights");
+  if (hidden == 32) {
+    // tensor-core weight image: fp16 hi/lo split-concatenated B' + f32 bias/readout
+    std::vector<uint8_t> img(tc::TILE_BYTES + 4 * (tc::GN + 32));
+    tc::pack_weights(Wx, Wh, b, w, img.data());
+    TS_CUDA(ctx->fast_w.reserve(img.size()));
+    TS_CUDA(cudaMemcpy(ctx->fast_w.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+  }
   return TS_OK;
 }
 
@@ -500,6 +509,40 @@ int ts_featurize_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records
   return check_device_status(ctx);
 }
 
+static size_t fast_pre_bytes(int T) { return sizeof(float) * (T + 1) * tc::PRE_STRIDE; }
+
+// Fast-path prefix (h, c, raw before every position of the all-unscheduled
+// sequence) computed by the tensor-core kernel itself, so replaying prefix
+// rows inside a tile is bit-identical to starting from the stored prefix.
+static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
+  if (P->fast_version == ctx->params_version) return TS_OK;
+  const int T = P->h->n_stages;
+  TS_CUDA(P->pre_fast.reserve(fast_pre_bytes(T) + sizeof(float) * T * F));
+  float* init32 = reinterpret_cast<float*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
+  {
+    const int64_t nw = (int64_t)T * F;
+    tc::k_rows32<<<(unsigned)((nw + 255) / 256), 256, 0, ctx->stream>>>(P->init_norm.as<double>(), nw, init32);
+    TS_LAUNCHED();
+  }
+  if (!ctx->tc_attr_set) {
+    TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+    ctx->tc_attr_set = true;
+  }
+  tc::TcArgs ta;
+  memset(&ta, 0, sizeof ta);
+  ta.wpack = ctx->fast_w.as<uint8_t>();
+  ta.init32 = init32;
+  ta.pre = P->pre_fast.as<float>();
+  ta.T = T;
+  ta.n_tiles = 1;
+  ta.record_prefix = 1;
+  ta.b_out = ctx->b_out;
+  tc::k_lstm_tc<<<1, tc::TM, tc::SMEM_BYTES, ctx->stream>>>(ta);
+  TS_LAUNCHED();
+  P->fast_version = ctx->params_version;
+  return TS_OK;
+}
+
 static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_records,
                         const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
                         double* d_out) {
@@ -510,7 +553,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1)));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
-      k_featurize_rows<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+      k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
       TS_LAUNCHED();
@@ -526,13 +569,53 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     return TS_OK;
   }
   if (mode == TS_MODE_FAST) {
-    rc = tc_score_states(ctx->stream, P->d.as<PipelineDesc>(), T, d_records, d_offsets, n_states,
-                         n_records, P->init_raw.as<double>(), P->init_norm.as<double>(),
-                         ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->fast_w.p, ctx->hidden,
-                         ctx->b_out, ctx->target_scale, ctx->params_version, &P->pre_fast.p,
-                         &P->pre_fast.bytes, &P->fast_version, &ctx->tmp.p, &ctx->tmp.bytes,
-                         &ctx->tmp2.p, &ctx->tmp2.bytes, ctx->status.as<int>(), d_out, &ctx->launches);
-    if (rc) return fail(ctx, rc, "fast path");
+    if (ctx->hidden != 32) return fail(ctx, TS_ERR_ARG, "the tensor-core path needs hidden = 32");
+    rc = ensure_fast_prefix(ctx, P);
+    if (rc) return rc;
+    // bucket states by depth (descending) so tiles share their depth
+    TS_CUDA(ctx->reps.reserve(sizeof(int) * (n_states + 2 * (T + 2))));
+    int* perm = ctx->reps.as<int>();
+    int* hist = perm + n_states;
+    int* cursor = hist + (T + 2);
+    const unsigned g = (unsigned)((n_states + 255) / 256);
+    {
+      KTimer kt(ctx, TS_K_OTHER);
+      TS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (T + 2), ctx->stream));
+      tc::k_depth_hist<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, hist);
+      TS_LAUNCHED();
+      tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor);
+      TS_LAUNCHED();
+      tc::k_depth_scatter<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, cursor, perm);
+      TS_LAUNCHED();
+    }
+    TS_CUDA(ctx->rows.reserve(sizeof(float) * F * (n_records > 0 ? n_records : 1)));
+    {
+      KTimer kt(ctx, TS_K_FEATURIZE);
+      k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>());
+      TS_LAUNCHED();
+    }
+    tc::TcArgs ta;
+    ta.wpack = ctx->fast_w.as<uint8_t>();
+    ta.init32 = reinterpret_cast<const float*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
+    ta.rows32 = ctx->rows.as<float>();
+    ta.offsets = d_offsets;
+    ta.perm = perm;
+    ta.pre = P->pre_fast.as<float>();
+    ta.out = d_out;
+    ta.n = n_states;
+    ta.T = T;
+    ta.n_tiles = (int)((n_states + tc::TM - 1) / tc::TM);
+    ta.record_prefix = 0;
+    ta.target_scale = ctx->target_scale;
+    ta.b_out = ctx->b_out;
+    {
+      KTimer kt(ctx, TS_K_LSTM_FAST);
+      const int grid = std::min(ta.n_tiles, ctx->sm_count * 3);
+      tc::k_lstm_tc<<<grid, tc::TM, tc::SMEM_BYTES, ctx->stream>>>(ta);
+      TS_LAUNCHED();
+    }
     return TS_OK;
   }
   return fail(ctx, TS_ERR_ARG, "unknown mode");

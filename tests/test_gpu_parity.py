@@ -130,3 +130,41 @@ def test_oracle_agrees_on_fresh_states(v0_path, v0, greedy_golden):
     feats = np.stack(featurize_states(states))
     for i, d in enumerate(decs):
         assert np.array_equal(bits(feats[i]), bits(O.features(P, d)))
+
+
+def test_fast_mode_position_and_batch_independence(state_sets, v0):
+    """Tiles replay the shared prefix: a state's FAST value must not depend on
+    which tile (depth mix) it lands in."""
+    z = state_sets["vgg16"]
+    p = pipeline_from(z)
+    states = product_states(p, z["keys"])
+    alone = np.array([predict_states(v0, [s], mode=MODE_FAST)[0] for s in states[:8]])
+    mixed = predict_states(v0, states[::-1] + states[:8] + states * 5, mode=MODE_FAST)
+    assert np.array_equal(bits(mixed[len(states): len(states) + 8]), bits(alone))
+    assert np.array_equal(bits(mixed[: len(states)][::-1][:8]), bits(alone))
+
+
+def test_fast_mode_large_batch_matches_exact(gpu_ctx, v0):
+    """1e5 device-generated VGG-16 states: FAST within 1e-4 of EXACT."""
+    import ctypes
+    import torch
+    p = pipeline_from({"text": (__import__("pathlib").Path(__file__).resolve().parent.parent
+                                / "assets/pipelines/nets/vgg16.pl").read_text()})
+    inf = ss._info(p)
+    pid = gpu_ctx.pipeline_id(inf.desc)
+    gpu_ctx.set_params(v0)
+    n = 100_000
+    recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
+    offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    nrec = ctypes.c_int64()
+    gpu_ctx.check(gpu_ctx.lib.ts_generate_states_device(gpu_ctx.h, pid, 777, n, recs.data_ptr(),
+                                                        offs.data_ptr(), ctypes.byref(nrec)))
+    out = {}
+    for mode in (MODE_EXACT, MODE_FAST):
+        o = torch.empty(n, dtype=torch.float64, device="cuda")
+        gpu_ctx.check(gpu_ctx.lib.ts_score_states_device(gpu_ctx.h, pid, recs.data_ptr(),
+                                                         offs.data_ptr(), n, nrec.value, mode,
+                                                         o.data_ptr()))
+        out[mode] = o.cpu().numpy()
+    assert np.all(out[MODE_EXACT] > 0)
+    np.testing.assert_allclose(out[MODE_FAST], out[MODE_EXACT], rtol=FAST_RTOL, atol=0)
