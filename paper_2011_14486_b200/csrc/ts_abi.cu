@@ -225,6 +225,12 @@ LstmW lstm_weights(ts_ctx* ctx) {
   return W;
 }
 
+// Dynamic shared memory for the featurize kernels' nest slots.
+size_t slot_smem(PipelineSlot* P, int block) {
+  const int ns = P->h->n_slots > 0 ? P->h->n_slots : 1;
+  return (size_t)ns * sizeof(Nest) * block;
+}
+
 // Init rows + exact prefix for the current parameters.
 int ensure_pipe_ready(ts_ctx* ctx, PipelineSlot* P) {
   if (!ctx->params_version) return fail(ctx, TS_ERR_STATE, "no parameters uploaded");
@@ -324,6 +330,20 @@ int ts_ctx_create(int device, ts_ctx** out) {
   if (e != cudaSuccess) {
     delete ctx;
     return TS_ERR_CUDA;
+  }
+  {
+    const int max_slot_smem = MAX_SLOTS * (int)sizeof(Nest) * 128;
+    e = cudaFuncSetAttribute(k_featurize_full, cudaFuncAttributeMaxDynamicSharedMemorySize, max_slot_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_featurize_rows<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               max_slot_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_featurize_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               max_slot_smem);
+    if (e != cudaSuccess) {
+      delete ctx;
+      return TS_ERR_CUDA;
+    }
   }
   const int rc = self_test(ctx);
   if (rc) {
@@ -428,6 +448,11 @@ int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* p
       }
     sd.slot = (int32_t)w[46];
     sd.n_splittable = (int32_t)w[47];
+    for (int k = 0; k < 8; ++k)
+      if (sd.ext[k] < 0 || sd.ext[k] >= (1ll << 31)) return fail(ctx, TS_ERR_PIPELINE, "extent >= 2^31");
+    if (sd.domain_points == 0) return fail(ctx, TS_ERR_PIPELINE, "empty domain");
+    sd.dp = make_divisor(sd.domain_points);
+    sd.io = make_divisor(1 + sd.i_in_bytes + sd.i_out_bytes);
     if (sd.consumer >= T || sd.slot >= n_slots || (sd.consumer >= 0 && sd.consumer <= s))
       return fail(ctx, TS_ERR_PIPELINE, "bad consumer/slot");
   }
@@ -471,7 +496,7 @@ int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh
   ++ctx->params_version;
   if (hidden == 32) {
     // tensor-core weight image: fp16 hi/lo split-concatenated B' + f32 bias/readout
-    std::vector<uint8_t> img(tc::TILE_BYTES + 4 * (tc::GN + 32));
+    std::vector<uint8_t> img(tc::TILE_BYTES + 4 * 32);
     tc::pack_weights(Wx, Wh, b, w, img.data());
     TS_CUDA(ctx->fast_w.reserve(img.size()));
     TS_CUDA(cudaMemcpy(ctx->fast_w.p, img.data(), img.size(), cudaMemcpyHostToDevice));
@@ -499,7 +524,7 @@ int ts_featurize_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records
                             ctx->stream));
   TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n_states + 1),
                           cudaMemcpyHostToDevice, ctx->stream));
-  k_featurize_full<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+  k_featurize_full<<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
       P->d.as<PipelineDesc>(), ctx->records.as<ts_decision>(), ctx->offsets.as<int64_t>(), n_states,
       P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), normalized,
       ctx->out.as<double>(), ctx->status.as<int>());
@@ -537,7 +562,9 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   ta.n_tiles = 1;
   ta.record_prefix = 1;
   ta.b_out = ctx->b_out;
-  tc::k_lstm_tc<<<1, tc::TM, tc::SMEM_BYTES, ctx->stream>>>(ta);
+  tc::k_prefix0<<<1, 64, 0, ctx->stream>>>(ta.pre, T, ctx->b_out);
+  TS_LAUNCHED();
+  tc::k_lstm_tc<<<1, tc::THREADS, tc::SMEM_BYTES, ctx->stream>>>(ta);
   TS_LAUNCHED();
   P->fast_version = ctx->params_version;
   return TS_OK;
@@ -553,7 +580,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1)));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
-      k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+      k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
       TS_LAUNCHED();
@@ -581,7 +608,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     {
       KTimer kt(ctx, TS_K_OTHER);
       TS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (T + 2), ctx->stream));
-      tc::k_depth_hist<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, hist);
+      tc::k_depth_hist<<<std::min<unsigned>(g, 4u * ctx->sm_count), 256, sizeof(int) * (T + 1), ctx->stream>>>(
+          d_offsets, n_states, T, hist);
       TS_LAUNCHED();
       tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor);
       TS_LAUNCHED();
@@ -591,7 +619,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     TS_CUDA(ctx->rows.reserve(sizeof(float) * F * (n_records > 0 ? n_records : 1)));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
-      k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
+      k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>());
       TS_LAUNCHED();
@@ -612,8 +640,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     ta.b_out = ctx->b_out;
     {
       KTimer kt(ctx, TS_K_LSTM_FAST);
-      const int grid = std::min(ta.n_tiles, ctx->sm_count * 3);
-      tc::k_lstm_tc<<<grid, tc::TM, tc::SMEM_BYTES, ctx->stream>>>(ta);
+      const int grid = std::min((ta.n_tiles + tc::NWG - 1) / tc::NWG, ctx->sm_count);
+      tc::k_lstm_tc<<<grid, tc::THREADS, tc::SMEM_BYTES, ctx->stream>>>(ta);
       TS_LAUNCHED();
     }
     return TS_OK;
@@ -713,7 +741,8 @@ static int host_nests(ts_ctx* ctx, const PipelineDesc& P, const ts_decision* pre
       cs = &P.st[sd.consumer];
       cn = &nests[sd.consumer];
     }
-    const int rc = build_nest(sd, cs, cn, d, nests[s]);
+    int64_t pe[TS_MAX_PURE];
+    const int rc = build_nest(sd, cs, cn, d, nests[s], pe);
     if (rc) return fail(ctx, rc, status_name(rc));
   }
   return TS_OK;
@@ -842,8 +871,9 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     if (epsilon > 0.0) rng += (uint64_t)n * 0x9E3779B97F4A7C15ull;
     vis += n;
     out_decisions[i] = cands[best];
+    int64_t pe[TS_MAX_PURE];
     const int brc = build_nest(sd, cands[best].anchor >= 0 ? cs : nullptr,
-                               cands[best].anchor >= 0 ? cn : nullptr, cands[best], nests[s]);
+                               cands[best].anchor >= 0 ? cn : nullptr, cands[best], nests[s], pe);
     if (brc) return fail(ctx, brc, status_name(brc));
     TS_CUDA(cudaMemcpyAsync(state_rows + (int64_t)s * F, ctx->rows.as<double>() + (int64_t)best * F,
                             sizeof(double) * F, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -868,6 +898,7 @@ int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int6
   int* depth = reinterpret_cast<int*>(fixed + n_states * T);
   k_generate<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
       P->d.as<PipelineDesc>(), seed0, n_states, fixed, depth, ctx->status.as<int>());
+  // (the generator keeps its nests in registers/local memory: untimed)
   TS_LAUNCHED();
   std::vector<int> hd(n_states);
   std::vector<int64_t> ho(n_states + 1);

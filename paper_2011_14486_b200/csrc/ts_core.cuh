@@ -146,6 +146,10 @@ TS_HD double glibc_log2(double x) {
 }
 
 // ------------------------------------------------------------ 256-bit ints
+// Invocation counts reach 133 bits on random VGG-16 states (inv*ppi 141,
+// SURVEY.md 7 hard part 4); 256 bits with an overflow status.  All limb
+// accesses use static indices (selects) so the device keeps them in
+// registers.
 struct u256 {
   uint64_t w[4];  // little-endian limbs
 };
@@ -157,6 +161,10 @@ TS_HD u256 u256_from(uint64_t v) {
   return r;
 }
 
+TS_HD uint64_t limb(const u256& a, int i) {
+  return i == 0 ? a.w[0] : i == 1 ? a.w[1] : i == 2 ? a.w[2] : i == 3 ? a.w[3] : 0;
+}
+
 TS_HD int clz64(uint64_t v) {
 #ifdef __CUDA_ARCH__
   return __clzll((long long)v);
@@ -165,17 +173,21 @@ TS_HD int clz64(uint64_t v) {
 #endif
 }
 
+TS_HD bool u256_small(const u256& a) { return (a.w[1] | a.w[2] | a.w[3]) == 0; }
+
 TS_HD int u256_bitlen(const u256& a) {
-  for (int i = 3; i >= 0; --i)
-    if (a.w[i]) return 64 * i + 64 - clz64(a.w[i]);
-  return 0;
+  return a.w[3] ? 256 - clz64(a.w[3])
+       : a.w[2] ? 192 - clz64(a.w[2])
+       : a.w[1] ? 128 - clz64(a.w[1])
+       : 64 - clz64(a.w[0]);
 }
 
 // a *= m; returns false on overflow past 256 bits
 TS_HD bool u256_mul_u64(u256& a, uint64_t m) {
   unsigned __int128 carry = 0;
+#pragma unroll
   for (int i = 0; i < 4; ++i) {
-    unsigned __int128 t = (unsigned __int128)a.w[i] * m + carry;
+    const unsigned __int128 t = (unsigned __int128)a.w[i] * m + carry;
     a.w[i] = (uint64_t)t;
     carry = t >> 64;
   }
@@ -184,129 +196,155 @@ TS_HD bool u256_mul_u64(u256& a, uint64_t m) {
 
 TS_HD bool u256_add_u64(u256& a, uint64_t v) {
   unsigned __int128 carry = v;
+#pragma unroll
   for (int i = 0; i < 4; ++i) {
-    unsigned __int128 t = (unsigned __int128)a.w[i] + carry;
+    const unsigned __int128 t = (unsigned __int128)a.w[i] + carry;
     a.w[i] = (uint64_t)t;
     carry = t >> 64;
   }
   return carry == 0;
 }
 
-// bits [lo, lo+64) of a (zero beyond 256)
+// bits [lo, lo+64) of a, lo in [0, 256)
 TS_HD uint64_t u256_bits64(const u256& a, int lo) {
-  if (lo >= 256) return 0;
-  if (lo < 0) {
-    // only used with lo >= -63: shift left
-    return a.w[0] << (-lo);
-  }
   const int li = lo >> 6, sh = lo & 63;
-  uint64_t v = a.w[li] >> sh;
-  if (sh && li + 1 < 4) v |= a.w[li + 1] << (64 - sh);
+  uint64_t v = limb(a, li) >> sh;
+  if (sh) v |= limb(a, li + 1) << (64 - sh);
   return v;
 }
 
-// true iff any bit below position `n` is set
+// true iff any bit below position n (0 <= n <= 256) is set
 TS_HD bool u256_any_below(const u256& a, int n) {
+  bool any = false;
+#pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int base = 64 * i;
-    if (n <= base) break;
-    if (n >= base + 64) {
-      if (a.w[i]) return true;
-    } else {
-      if (a.w[i] & ((1ull << (n - base)) - 1)) return true;
-    }
+    const uint64_t m = n >= base + 64 ? ~0ull : (n <= base ? 0ull : ((1ull << (n - base)) - 1));
+    any = any || (a.w[i] & m);
   }
-  return false;
+  return any;
 }
 
-TS_HD u256 u256_shl(const u256& a, int s) {
-  u256 r = u256_from(0);
+TS_HD u256 u256_shl(const u256& a, int s) {  // 0 <= s < 256
+  u256 r;
   const int li = s >> 6, sh = s & 63;
-  for (int i = 3; i >= li; --i) {
-    uint64_t v = a.w[i - li] << sh;
-    if (sh && i - li - 1 >= 0) v |= a.w[i - li - 1] >> (64 - sh);
-    r.w[i] = v;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint64_t v = limb(a, i - li) << sh;
+    if (sh) v |= limb(a, i - li - 1) >> (64 - sh);
+    r.w[i] = (i - li >= 0) ? v : 0;
   }
   return r;
 }
 
-// Builds the double mant * 2^e2 for a 53-bit mant in [2^52, 2^53] (exact).
+TS_HD double u64_to_double(uint64_t v) {  // round to nearest even
+#ifdef __CUDA_ARCH__
+  return __ull2double_rn(v);
+#else
+  return (double)v;
+#endif
+}
+
+// mant (53 bits, top bit at 52, or exactly 2^53 after rounding) * 2^e2, exact
 TS_HD double make_double(uint64_t mant, int e2) {
   if (mant == (1ull << 53)) {
     mant >>= 1;
     e2 += 1;
   }
-  // value = mant * 2^e2, mant has its top bit at 52 -> exponent e2 + 52
   const int64_t biased = (int64_t)e2 + 52 + 1023;
   if (biased >= 2047) return 1.0 / 0.0;
-  if (biased <= 0) {
-    // subnormal: cannot happen for the quantities on this path; fall back
-    // to an exact-as-possible scaling (flag via caller bounds)
-    double d = (double)mant;
-    for (int i = 0; i < -e2; ++i) d = fmul(d, 0.5);
-    return d;
-  }
+  if (biased <= 0) return 0.0;  // subnormal quotients do not occur on this path
   return as_double(((uint64_t)biased << 52) | (mant & ((1ull << 52) - 1)));
 }
 
-// Round the integer (q, sticky) - value q + f with 0 <= f < 1 and f > 0 iff
-// sticky - to 53 bits half-even, scaled by 2^e2.
+// Round q + f (0 <= f < 1, f > 0 iff sticky) to 53 bits half-even, times
+// 2^e2.  Callers guarantee q has >= 55 bits whenever sticky is set.
 TS_HD double round_u256(const u256& q, bool sticky, int e2) {
   const int bl = u256_bitlen(q);
   if (bl == 0) return 0.0;
-  if (bl <= 53 && !sticky) {
-    const uint64_t m = q.w[0];
-    const int norm = 53 - bl;
-    return make_double(m << norm, e2 - norm);
-  }
   if (bl <= 53) {
-    // fraction bits below the integer: caller guarantees bl >= 55 when
-    // sticky is set, so this branch is unreachable in practice
-    const uint64_t m = q.w[0];
     const int norm = 53 - bl;
-    return make_double(m << norm, e2 - norm);
+    return make_double(q.w[0] << norm, e2 - norm);
   }
   const int sh = bl - 53;
-  uint64_t mant = u256_bits64(q, sh) & ((1ull << 53) - 1);
-  mant |= (1ull << 52);
-  // rounding: bit sh-1 is the half bit, below it + sticky decide
+  uint64_t mant = (u256_bits64(q, sh) & ((1ull << 53) - 1)) | (1ull << 52);
   const bool half = (u256_bits64(q, sh - 1) & 1ull) != 0;
-  const bool below = u256_any_below(q, sh - 1) || sticky;
+  const bool below = sticky || u256_any_below(q, sh - 1);
   if (half && (below || (mant & 1ull))) mant += 1;
   return make_double(mant, e2 + sh);
 }
 
 // PyLong_AsDouble: correctly rounded, ties to even.
-TS_HD double u256_to_double(const u256& a) { return round_u256(a, false, 0); }
+TS_HD double u256_to_double(const u256& a) {
+  if (u256_small(a)) return u64_to_double(a.w[0]);
+  return round_u256(a, false, 0);
+}
 
-// q = a / d, r = a % d (d > 0)
-TS_HD u256 u256_divmod_u64(const u256& a, uint64_t d, uint64_t& rem) {
-  u256 q;
-  unsigned __int128 r = 0;
-  for (int i = 3; i >= 0; --i) {
-    const unsigned __int128 cur = (r << 64) | a.w[i];
-    q.w[i] = (uint64_t)(cur / d);
-    r = cur % d;
+// Division by an invariant normalized divisor with a precomputed reciprocal
+// (Moller & Granlund 2011, "Improved division by invariant integers",
+// Alg. 4): (u1:u0) / d with u1 < d, d >= 2^63, v = floor((2^128-1)/d) - 2^64.
+TS_HD uint64_t div2by1(uint64_t u1, uint64_t u0, uint64_t d, uint64_t v, uint64_t& r) {
+  unsigned __int128 q = (unsigned __int128)v * u1;
+  q += ((unsigned __int128)(u1 + 1) << 64) | u0;
+  uint64_t q1 = (uint64_t)(q >> 64);
+  const uint64_t q0 = (uint64_t)q;
+  uint64_t rr = u0 - q1 * d;
+  if (rr > q0) {
+    q1 -= 1;
+    rr += d;
   }
-  rem = (uint64_t)r;
+  if (rr >= d) {
+    q1 += 1;
+    rr -= d;
+  }
+  r = rr;
+  return q1;
+}
+
+// Invariant divisor: d = dn >> shift with dn normalized; inv from host.
+struct Divisor {
+  uint64_t d, dn, inv;
+  int32_t shift;
+};
+
+inline Divisor make_divisor(uint64_t d) {  // host-side precomputation
+  Divisor D;
+  D.d = d;
+  D.shift = clz64(d);
+  D.dn = d << D.shift;
+  D.inv = (uint64_t)((~(unsigned __int128)0) / D.dn - ((unsigned __int128)1 << 64));
+  return D;
+}
+
+// q = a / d (quotient, 256 bits), returns whether the remainder is nonzero
+TS_HD u256 u256_div(const u256& a, const Divisor& D, bool& inexact) {
+  const int s = D.shift;
+  // dividend << s as five limbs n4..n0
+  uint64_t n[5];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) n[i] = s ? (a.w[i] << s) | (i ? a.w[i - 1] >> (64 - s) : 0) : a.w[i];
+  n[4] = s ? a.w[3] >> (64 - s) : 0;
+  uint64_t r = n[4];
+  u256 q;
+#pragma unroll
+  for (int i = 3; i >= 0; --i) q.w[i] = div2by1(r, n[i], D.dn, D.inv, r);
+  inexact = r != 0;
   return q;
 }
 
 // CPython int/int true division (long_true_divide): correctly rounded n/d.
-TS_HD double u256_div_u64_to_double(const u256& n, uint64_t d) {
+TS_HD double u256_div_to_double(const u256& n, const Divisor& D) {
+  if (u256_small(n) && n.w[0] <= (1ull << 53) && D.d <= (1ull << 53))
+    return fdiv(u64_to_double(n.w[0]), u64_to_double(D.d));  // both exact: IEEE division
   const int a = u256_bitlen(n);
   if (a == 0) return 0.0;
-  const int b = 64 - clz64(d);
+  const int b = 64 - clz64(D.d);
   int k = 55 + b - a;  // scale so the quotient carries >= 55 bits
-  u256 N = n;
-  if (k > 0) {
-    N = u256_shl(n, k);
-  } else {
-    k = 0;
-  }
-  uint64_t rem;
-  const u256 q = u256_divmod_u64(N, d, rem);
-  return round_u256(q, rem != 0, -k);
+  const u256 N = k > 0 ? u256_shl(n, k) : n;
+  if (k < 0) k = 0;
+  bool inexact;
+  const u256 q = u256_div(N, D, inexact);
+  return round_u256(q, inexact, -k);
 }
 
 // ------------------------------------------------------------ descriptor
@@ -317,6 +355,8 @@ struct StageDesc {
   uint64_t pure_points;                   // prod of pure extents
   uint64_t red_points;                    // prod of reduction extents
   uint64_t domain_points;                 // pure_points * red_points
+  Divisor dp;                             // domain_points as an invariant divisor
+  Divisor io;                             // 1 + input_bytes + output_bytes
   // schedule-invariant integers (pipeline_ir.py:241-252)
   uint64_t i_points, i_flops, i_in_bytes, i_out_bytes;
   int32_t n_inputs;
@@ -337,32 +377,34 @@ struct PipelineDesc {
 };
 
 // ------------------------------------------------------------------ nests
-// Materialized loops of one scheduled stage (schedule_space.py:118-128).
+// Materialized loops of one scheduled stage (schedule_space.py:118-128),
+// compact (80 bytes): what a producer anchored here needs.
 struct Nest {
-  u256 inv;                    // invocations
-  int64_t pe[TS_MAX_PURE];     // per-invocation pure extents
-  int64_t ext[TS_MAX_LOOPS];   // loop extents outermost first
-  uint8_t id[TS_MAX_LOOPS];    // loop ids (ts_decision.order encoding)
+  u256 inv;                   // invocations
+  uint32_t ext[TS_MAX_LOOPS]; // loop extents outermost first (< 2^31, descriptor-checked)
+  uint8_t id[TS_MAX_LOOPS];   // loop ids (ts_decision.order encoding)
   int32_t n_loops;
   int32_t depth;
 };
 
 TS_HD int loop_dim(uint8_t id, int n_pure) { return id < 8 ? (id >> 1) : n_pure + (id - 8); }
 
+TS_HD int64_t sel4(const int64_t* a, int k) { return k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : a[3]; }
+
 // _anchor_ok (schedule_space.py:176-187): a level is illegal if it sits
 // between the inner and the outer loop of a split dim.
 TS_HD bool anchor_ok(const Nest& c, int lvl) {
-  for (int j = 0; j < c.n_loops; ++j) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j) {
     const uint8_t id = c.id[j];
-    if (id < 8 && (id & 1)) {  // inner loop of split dim (id>>1)
-      const int pi = j;
-      int po = -1;
-      for (int t = 0; t < c.n_loops; ++t)
-        if (c.id[t] == (uint8_t)(id - 1)) po = t;
-      if (po >= 0 && pi <= lvl && lvl < po) return false;
+    if (j < c.n_loops && id < 8 && (id & 1) && j <= lvl) {  // inner loop at or above lvl
+#pragma unroll
+      for (int t = 0; t < TS_MAX_LOOPS; ++t)
+        if (t < c.n_loops && c.id[t] == (uint8_t)(id - 1) && lvl < t) ok = false;
     }
   }
-  return true;
+  return ok;
 }
 
 // Per-invocation pure extents, invocations and depth of stage `s` anchored
@@ -371,64 +413,87 @@ TS_HD bool anchor_ok(const Nest& c, int lvl) {
 TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& cn, int lvl,
                            int64_t* pe, u256& inv, int& depth) {
   inv = cn.inv;
-  for (int j = 0; j <= lvl; ++j)
-    if (!u256_mul_u64(inv, (uint64_t)cn.ext[j])) return TS_ERR_OVERFLOW;
+  bool ok = true;
   int64_t rem[TS_MAX_PURE + TS_MAX_RED];
-  const int cdims = cs.n_pure + cs.n_red;
-  for (int d = 0; d < cdims; ++d) rem[d] = 1;
-  for (int j = lvl + 1; j < cn.n_loops; ++j) rem[loop_dim(cn.id[j], cs.n_pure)] *= cn.ext[j];
-  for (int k = 0; k < s.n_pure; ++k) {
+#pragma unroll
+  for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd) rem[dd] = 1;
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j) {
+    if (j >= cn.n_loops) continue;
+    if (j <= lvl) {
+      ok = u256_mul_u64(inv, cn.ext[j]) && ok;
+    } else {
+      const int dim = loop_dim(cn.id[j], cs.n_pure);
+#pragma unroll
+      for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd)
+        if (dd == dim) rem[dd] *= cn.ext[j];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < TS_MAX_PURE; ++k) {
     int64_t best = -1;
-    for (int e = 0; e < s.n_cedges; ++e) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      if (e >= s.n_cedges) continue;
       const int cd = s.cdim[e][k];
-      const int64_t ext = cd < 0 ? s.cwindow[e][k] : s.cstride[e][k] * (rem[cd] - 1) + s.cwindow[e][k];
-      if (ext > best) best = ext;
+      int64_t rv = 1;
+#pragma unroll
+      for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd)
+        if (dd == cd) rv = rem[dd];
+      const int64_t ext = cd < 0 ? s.cwindow[e][k] : s.cstride[e][k] * (rv - 1) + s.cwindow[e][k];
+      best = ext > best ? ext : best;
     }
     pe[k] = best;
   }
   depth = cn.depth + lvl + 1;
-  return TS_OK;
+  return ok ? TS_OK : TS_ERR_OVERFLOW;
 }
 
 // _nest_entry/_build_loops (schedule_space.py:228-274).  `cn` may be null
-// for Root decisions.  Returns a ts_status.
+// for Root decisions; pe receives the per-invocation pure extents.
 TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const Nest* cn, const ts_decision& d,
-                     Nest& out) {
+                     Nest& out, int64_t* pe) {
   if (d.anchor >= 0) {
     if (!cn || !cs || d.anchor >= cn->n_loops) return TS_ERR_ILLEGAL;
-    const int rc = anchored_extents(s, *cs, *cn, d.anchor, out.pe, out.inv, out.depth);
+    const int rc = anchored_extents(s, *cs, *cn, d.anchor, pe, out.inv, out.depth);
     if (rc) return rc;
   } else {
-    for (int k = 0; k < s.n_pure; ++k) out.pe[k] = s.ext[k];
+#pragma unroll
+    for (int k = 0; k < TS_MAX_PURE; ++k) pe[k] = s.ext[k];
     out.inv = u256_from(1);
     out.depth = 0;
   }
   if (d.n_loops == 0 || d.n_loops > TS_MAX_LOOPS) return TS_ERR_ILLEGAL;
   out.n_loops = d.n_loops;
-  for (int j = 0; j < d.n_loops; ++j) {
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j) {
     const uint8_t id = d.order[j];
     out.id[j] = id;
+    if (j >= d.n_loops) {
+      out.ext[j] = 0;
+      continue;
+    }
+    int64_t e;
     if (id < 8) {
       const int k = id >> 1;
-      if (k >= s.n_pure) return TS_ERR_ILLEGAL;
-      const int64_t f = d.split[k];
-      if (f) {
-        out.ext[j] = (id & 1) ? f : out.pe[k] / f;
-      } else {
-        if (id & 1) return TS_ERR_ILLEGAL;
-        out.ext[j] = out.pe[k];
-      }
+      const int64_t f = k == 0 ? d.split[0] : k == 1 ? d.split[1] : k == 2 ? d.split[2] : d.split[3];
+      const int64_t p = sel4(pe, k);
+      bad = bad || k >= s.n_pure || (!f && (id & 1));
+      e = f ? ((id & 1) ? f : p / f) : p;
     } else {
       const int r = id - 8;
-      if (r >= s.n_red) return TS_ERR_ILLEGAL;
-      out.ext[j] = s.ext[s.n_pure + r];
+      bad = bad || r >= s.n_red;
+      e = r == 0 ? s.ext[s.n_pure] : r == 1 ? s.ext[s.n_pure + 1] : r == 2 ? s.ext[s.n_pure + 2]
+                                                                            : s.ext[s.n_pure + 3];
     }
+    out.ext[j] = (uint32_t)e;
   }
-  return TS_OK;
+  return bad ? TS_ERR_ILLEGAL : TS_OK;
 }
 
 // check_action (schedule_space.py:288-347) on an encoded decision: null if
-// legal, else the violated invariant.
+// legal, else the violated invariant.  Host only.
 inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const Nest* cn,
                                   const ts_decision& d) {
   if (d.anchor >= 0) {
@@ -471,7 +536,8 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
     if (seen[id]++) return "order is not a permutation of the stage's loops";
   }
   Nest n;
-  if (build_nest(s, cs, cn, d, n)) return "order is not a permutation of the stage's loops";
+  int64_t pe2[TS_MAX_PURE];
+  if (build_nest(s, cs, cn, d, n, pe2)) return "order is not a permutation of the stage's loops";
   if (!(d.vec == 1 || d.vec == 4 || d.vec == 8 || d.vec == 16)) return "bad vectorize width";
   if (d.vec > 1) {
     if (n.id[n.n_loops - 1] >= 8) return "vectorized loop is a reduction dim";
@@ -483,23 +549,30 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
 
 // Acquired features f8..f15 of a scheduled stage (featurizer.py:86-103),
 // raw (not normalized).
-TS_HD int acquired_features(const StageDesc& s, const Nest& n, const ts_decision& d, double* f) {
+TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe, const ts_decision& d,
+                            double* f) {
+  uint32_t inner = 0;
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j)
+    if (j == n.n_loops - 1) inner = n.ext[j];
   f[0] = 1.0;
   f[1] = glibc_log2((double)d.vec);
   f[2] = (d.flags & TS_FLAG_PARALLEL) ? glibc_log2((double)n.ext[0]) : 0.0;
-  f[3] = glibc_log2((double)n.ext[n.n_loops - 1]);
+  f[3] = glibc_log2((double)inner);
   f[4] = (double)n.depth;
   // recompute factor = Fraction(inv * ppi, domain_points)  (cost_oracle.py:108-121)
   uint64_t region = 1;
-  for (int k = 0; k < s.n_pure; ++k) region *= (uint64_t)n.pe[k];
+#pragma unroll
+  for (int k = 0; k < TS_MAX_PURE; ++k)
+    if (k < s.n_pure) region *= (uint64_t)pe[k];
   u256 num = n.inv;
-  if (!u256_mul_u64(num, region)) return TS_ERR_OVERFLOW;
-  if (!u256_mul_u64(num, s.red_points)) return TS_ERR_OVERFLOW;
-  f[5] = glibc_log2(u256_div_u64_to_double(num, s.domain_points));
+  bool ok = u256_mul_u64(num, region);
+  ok = u256_mul_u64(num, s.red_points) && ok;
+  if (!ok) return TS_ERR_OVERFLOW;
+  f[5] = glibc_log2(u256_div_to_double(num, s.dp));
   // working set at the store site (cost_oracle.py:162-169), cache 32768
   const uint64_t pts = (d.flags & TS_FLAG_STORE_AT) ? region : s.pure_points;
-  const unsigned __int128 ws = (unsigned __int128)pts * 4u;
-  f[6] = ws <= 32768u ? 1.0 : 0.0;
+  f[6] = pts <= 8192u ? 1.0 : 0.0;  // 4 * pts <= 32768, overflow-free
   u256 inv1 = n.inv;
   if (!u256_add_u64(inv1, 1)) return TS_ERR_OVERFLOW;
   f[7] = glibc_log2(u256_to_double(inv1));
@@ -512,7 +585,7 @@ TS_HD void intrinsic_features(const StageDesc& s, double* f) {
   f[1] = glibc_log2(u256_to_double(u256_from(s.i_flops + 1)));
   f[2] = glibc_log2(u256_to_double(u256_from(s.i_in_bytes + 1)));
   f[3] = glibc_log2(u256_to_double(u256_from(s.i_out_bytes + 1)));
-  f[4] = u256_div_u64_to_double(u256_from(s.i_flops), 1 + s.i_in_bytes + s.i_out_bytes);
+  f[4] = u256_div_to_double(u256_from(s.i_flops), s.io);
   f[5] = (double)s.n_inputs;
   f[6] = (double)s.n_red;
   f[7] = s.ov_window ? fdiv((double)s.ov_window, (double)(s.ov_stride > 1 ? s.ov_stride : 1)) : 0.0;

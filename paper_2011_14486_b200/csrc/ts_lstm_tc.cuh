@@ -3,17 +3,24 @@
 // cell update, readout and exp.
 //
 // Per timestep each row (one state) computes z = [x | h] . [Wx; Wh] + b, a
-// [1 x 48] x [48 x 128] product.  A CTA stacks 128 states as the M=128 rows
-// of one UMMA: D[128 x 128] (fp32, TMEM) = A[128 x K] . B[128 x K]^T with
-// fp16 operands split hi/lo and concatenated along K,
-//     A' = [a_hi | a_lo | a_hi],  B' = [W_hi ; W_hi ; W_lo]   (K = 3*48 = 144)
-// so a.W ~= a_hi W_hi + a_lo W_hi + a_hi W_lo with 22-bit operands and fp32
-// accumulation (|dV|/V <= 1e-4, the north-star fp32 tolerance).  9 UMMAs of
-// K=16 per timestep, issued by one thread, completion via tcgen05.commit on
-// an mbarrier; the 128 epilogue threads (thread = TMEM lane = state) read
-// their row with tcgen05.ld, apply the gates in fp32 (MUFU ex2/rcp), update
-// c (registers) and h, and write the next A row (fp16 hi/lo) to shared
-// memory in the canonical K-major no-swizzle layout.
+// [1 x 48] x [48 x 128] product.  A warpgroup stacks 128 states as the
+// M=128 rows of one UMMA: D[128 x 128] (fp32, TMEM) = A[128 x K] . B[128 x K]^T
+// with fp16 operands split hi/lo and concatenated along K,
+//     A' = [a_hi | a_lo | a_hi | 1 1 0..0],  B' = [W_hi ; W_hi ; W_lo ; b_hi b_lo 0..0]
+// (K = 3*48 + 16 = 160, ten K=16 UMMAs) so z ~= a_hi W_hi + a_lo W_hi + a_hi W_lo + b
+// with 22-bit operands and fp32 accumulation (|dV|/V <= 1e-4, the north-star
+// fp32 tolerance).  The gate columns of B' are pre-scaled by -log2(e)
+// (i, f, o) and -2 log2(e) (g) so every gate costs one ex2.approx and one
+// rcp.approx on the MUFU pipe: sigma = 1/(1 + 2^u), tanh = 2/(1 + 2^v) - 1.
+//
+// A CTA holds NWG = 4 warpgroups (512 threads, one CTA per SM) that share the
+// weight tile B' in shared memory and own one A tile, one 128-column TMEM
+// accumulator and one mbarrier each; they run independent tiles so one
+// warpgroup's UMMA + commit latency hides under the others' MUFU work.
+// One elected thread per warpgroup issues the UMMAs; tcgen05.commit arrives
+// on the warpgroup's mbarrier; thread = TMEM lane = state reads its row with
+// tcgen05.ld, updates c (registers), h, the readout, and writes the next A
+// row (fp16 hi/lo) in the canonical K-major no-swizzle layout.
 //
 // Batch independence: every row's arithmetic depends only on its own inputs,
 // so a state of depth d in a tile that starts earlier (at T - d_max) replays
@@ -33,12 +40,16 @@ namespace tc {
 constexpr int TM = 128;                   // states per tile (UMMA M)
 constexpr int GN = 128;                   // gate columns 4H (UMMA N), H = 32
 constexpr int KA = 48;                    // [x(16) | h(32)]
-constexpr int KP = 3 * KA;                // split-concatenated K = 144
-constexpr int KCH = KP / 8;               // 16-byte K chunks = 18
+constexpr int KP = 3 * KA + 16;           // split-concatenated K + bias block = 160
+constexpr int KCH = KP / 8;               // 16-byte K chunks = 20
+constexpr int KSTEPS = KP / 16;           // UMMAs per timestep = 10
 constexpr int CHUNK_STRIDE = TM * 16;     // bytes between K chunks (LBO) = 2048
-constexpr int TILE_BYTES = KCH * CHUNK_STRIDE;  // 36864 per operand
-constexpr int SMEM_BYTES = 2 * TILE_BYTES + 1024 + 1024;  // A, B, bias/readout, barriers
-constexpr int PRE_STRIDE = 72;            // floats per prefix position: h[32], c[32], raw (as 2 floats) ...
+constexpr int TILE_BYTES = KCH * CHUNK_STRIDE;  // 40960 per operand
+constexpr int NWG = 4;                    // warpgroups (tiles in flight) per CTA
+constexpr int THREADS = NWG * TM;
+constexpr int SMEM_BYTES = (1 + NWG) * TILE_BYTES + 1024;  // B, NWG x A, readout + barriers
+constexpr int PRE_STRIDE = 72;            // floats per prefix position: h[32], c[32], raw (f64)
+constexpr float LOG2E = 1.4426950408889634f;
 
 // ------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -85,6 +96,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void wg_sync(int wg) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + wg), "r"(TM) : "memory");
+}
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
@@ -98,29 +112,41 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- epilogue
-__device__ __forceinline__ float sig_f(float x) { return __frcp_rn(1.0f + __expf(-x)); }
-__device__ __forceinline__ float tanh_f(float x) { return fmaf(2.0f, sig_f(2.0f * x), -1.0f); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// u = -z log2 e  ->  sigma(z);   v = -2 z log2 e  ->  tanh(z)
+__device__ __forceinline__ float sig_u(float u) { return rcp(1.0f + ex2(u)); }
+__device__ __forceinline__ float tanh_v(float v) { return fmaf(2.0f, rcp(1.0f + ex2(v)), -1.0f); }
 
 // hi/lo fp16 split of 8 floats into two 16-byte chunks
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
-  __half2 h[4], l[4];
+  uint32_t h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const __half a = __float2half_rn(v[2 * i]), b = __float2half_rn(v[2 * i + 1]);
-    h[i] = __halves2half2(a, b);
-    l[i] = __halves2half2(__float2half_rn(v[2 * i] - __half2float(a)),
-                          __float2half_rn(v[2 * i + 1] - __half2float(b)));
+    const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+    const float2 back = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(v[2 * i] - back.x, v[2 * i + 1] - back.y);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
   }
-  hi = *reinterpret_cast<uint4*>(h);
-  lo = *reinterpret_cast<uint4*>(l);
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-// Stores a 16-byte chunk `kc` of row `r` in the canonical no-swizzle layout.
+// Stores 16-byte chunk `kc` of row `r` in the canonical no-swizzle layout.
 __device__ __forceinline__ void st_chunk(uint8_t* A, int kc, int r, const uint4& v) {
   *reinterpret_cast<uint4*>(A + kc * CHUNK_STRIDE + (r >> 3) * 128 + (r & 7) * 16) = v;
 }
 
-// Writes the x part (chunks q=0,1 of every segment) of row r.
+// x part: chunks q = 0, 1 of every segment
 __device__ __forceinline__ void put_x(uint8_t* A, int r, const float* x) {
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -132,16 +158,20 @@ __device__ __forceinline__ void put_x(uint8_t* A, int r, const float* x) {
   }
 }
 
-// Writes the h part (chunks q=2..5) of row r.
-__device__ __forceinline__ void put_h(uint8_t* A, int r, const float* h) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 hi, lo;
-    split8(h + 8 * q, hi, lo);
-    st_chunk(A, 0 * 6 + 2 + q, r, hi);
-    st_chunk(A, 1 * 6 + 2 + q, r, lo);
-    st_chunk(A, 2 * 6 + 2 + q, r, hi);
-  }
+// h part: 8 units of group g8 -> chunk q = 2 + g8 of every segment
+__device__ __forceinline__ void put_h8(uint8_t* A, int r, int g8, const float* h8) {
+  uint4 hi, lo;
+  split8(h8, hi, lo);
+  st_chunk(A, 0 * 6 + 2 + g8, r, hi);
+  st_chunk(A, 1 * 6 + 2 + g8, r, lo);
+  st_chunk(A, 2 * 6 + 2 + g8, r, hi);
+}
+
+// bias block: K entries 144, 145 = 1.0 (multiplying b_hi, b_lo), rest 0
+__device__ __forceinline__ void put_bias_ones(uint8_t* A, int r) {
+  const uint32_t one_one = 0x3C003C00u;  // two fp16 1.0
+  st_chunk(A, 18, r, make_uint4(one_one, 0u, 0u, 0u));
+  st_chunk(A, 19, r, make_uint4(0u, 0u, 0u, 0u));
 }
 
 // ---------------------------------------------------------------- kernel
@@ -151,12 +181,12 @@ __device__ __forceinline__ void put_h(uint8_t* A, int r, const float* h) {
 // whose row 0 is the all-unscheduled state (depth 0, t0 = 0); thread 0
 // writes (h, c, raw) before every timestep into `pre` (the fast prefix).
 struct TcArgs {
-  const uint8_t* wpack;     // B' image (TILE_BYTES) + bias[128] f32 + w[32] f32
+  const uint8_t* wpack;     // B' image (TILE_BYTES) + readout w[32] f32
   const float* init32;      // [T][16] normalized unscheduled rows (fp32)
   const float* rows32;      // [n_records][16] normalized scheduled rows (fp32)
   const int64_t* offsets;   // [n+1]
   const int* perm;          // [n] sorted position -> state
-  float* pre;               // [(T+1)][PRE_STRIDE] fast prefix (h, c, raw hi/lo)
+  float* pre;               // [(T+1)][PRE_STRIDE] fast prefix (h, c, raw)
   double* out;              // [n] V
   int64_t n;
   int T;
@@ -166,47 +196,61 @@ struct TcArgs {
   double b_out;
 };
 
-__global__ void __launch_bounds__(TM, 1) k_lstm_tc(TcArgs a) {
+__device__ __forceinline__ void load_x(const float* src, float* x) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 v = __ldg(s4 + q);
+    x[4 * q] = v.x;
+    x[4 * q + 1] = v.y;
+    x[4 * q + 2] = v.z;
+    x[4 * q + 3] = v.w;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* A = smem;
-  uint8_t* B = smem + TILE_BYTES;
-  float* bias = reinterpret_cast<float*>(smem + 2 * TILE_BYTES);  // [128]
-  float* wout = bias + GN;                                       // [32]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * TILE_BYTES + 1024);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int r = threadIdx.x;
-  const int warp = r >> 5;
+  uint8_t* B = smem;
+  const int tid = threadIdx.x;
+  const int wg = tid / TM;            // warpgroup
+  const int r = tid % TM;             // row within the tile = TMEM lane
+  const int warp = tid >> 5;
+  uint8_t* A = smem + (1 + wg) * TILE_BYTES;
+  float* wout = reinterpret_cast<float*>(smem + (1 + NWG) * TILE_BYTES);  // [32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wout + 64);               // [NWG]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
 
   // weights -> shared (B' image is already in the canonical layout)
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.wpack);
     uint4* dst = reinterpret_cast<uint4*>(B);
-    for (int i = r; i < TILE_BYTES / 16; i += TM) dst[i] = __ldg(src + i);
-    const float* fb = reinterpret_cast<const float*>(a.wpack + TILE_BYTES);
-    bias[r] = __ldg(fb + r);
-    if (r < 32) wout[r] = __ldg(fb + GN + r);
+    for (int i = tid; i < TILE_BYTES / 16; i += THREADS) dst[i] = __ldg(src + i);
+    if (tid < 32) wout[tid] = __ldg(reinterpret_cast<const float*>(a.wpack + TILE_BYTES) + tid);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(128)
+                 "r"(NWG * 128)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (r == 0) {
-    mbar_init(bar, 1);
+  if (tid == 0) {
+    for (int g = 0; g < NWG; ++g) mbar_init(bars + g, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = *tmem_slot + wg * 128;   // this warpgroup's 128 columns
+  const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const uint32_t a_base = smem_u32(A), b_base = smem_u32(B);
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  uint64_t* bar = bars + wg;
   uint32_t phase = 0;
   const int T = a.T;
+  const float c2 = -2.0f * LOG2E;
+  put_bias_ones(A, r);
 
-  for (int tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
+  for (int tile = blockIdx.x * NWG + wg; tile < a.n_tiles; tile += gridDim.x * NWG) {
     const int64_t sp = (int64_t)tile * TM + r;
     const bool valid = a.record_prefix ? (r == 0) : (sp < a.n);
     int64_t st = 0, off = 0;
@@ -216,110 +260,105 @@ __global__ void __launch_bounds__(TM, 1) k_lstm_tc(TcArgs a) {
       off = a.offsets[st];
       d = (int)(a.offsets[st + 1] - off);
     }
-    int dmax;
-    if (a.record_prefix) {
-      dmax = 0;
-    } else {
+    int dmax = T;  // record pass: the all-unscheduled row runs every timestep
+    if (!a.record_prefix) {
       const int64_t first = a.perm[(int64_t)tile * TM];
       dmax = (int)(a.offsets[first + 1] - a.offsets[first]);
     }
-    const int t0 = a.record_prefix ? 0 : T - dmax;
-    float h[32], c[32];
+    const int t0 = T - dmax;
+    float c[32];
     double raw;
-    if (a.record_prefix) {
+    {
+      float h0[32];
+      if (a.record_prefix) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) h[j] = c[j] = 0.0f;
-      raw = fmul((double)T, a.b_out);
-    } else {
-      const float* p = a.pre + (int64_t)t0 * PRE_STRIDE;
+        for (int j = 0; j < 32; ++j) h0[j] = c[j] = 0.0f;
+        raw = fmul((double)T, a.b_out);
+      } else {
+        const float* p = a.pre + (int64_t)t0 * PRE_STRIDE;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        h[j] = p[j];
-        c[j] = p[32 + j];
-      }
-      raw = *reinterpret_cast<const double*>(p + 64);
-    }
-    put_h(A, r, h);
-    for (int t = t0; t < T; ++t) {
-      if (a.record_prefix && r == 0) {
-        float* p = a.pre + (int64_t)t * PRE_STRIDE;
         for (int j = 0; j < 32; ++j) {
-          p[j] = h[j];
-          p[32 + j] = c[j];
+          h0[j] = p[j];
+          c[j] = p[32 + j];
         }
-        *reinterpret_cast<double*>(p + 64) = raw;
+        raw = *reinterpret_cast<const double*>(p + 64);
       }
-      // x row for this timestep: own scheduled row or the shared prefix row
-      float x[16];
-      const float* src = (t < T - d) ? a.init32 + t * 16 : a.rows32 + (off + (T - 1 - t)) * 16;
-      const float4* s4 = reinterpret_cast<const float4*>(src);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 v = __ldg(s4 + q);
-        x[4 * q] = v.x;
-        x[4 * q + 1] = v.y;
-        x[4 * q + 2] = v.z;
-        x[4 * q + 3] = v.w;
-      }
+      for (int g8 = 0; g8 < 4; ++g8) put_h8(A, r, g8, h0 + 8 * g8);
+    }
+    float x[16];
+    load_x((t0 < T - d) ? a.init32 + t0 * 16 : a.rows32 + (off + (T - 1 - t0)) * 16, x);
+    for (int t = t0; t < T; ++t) {
       put_x(A, r, x);
       fence_async_smem();
       fence_before();
-      __syncthreads();
+      wg_sync(wg);
       if (r == 0) {
         fence_after();
 #pragma unroll
-        for (int s = 0; s < KCH / 2; ++s)
+        for (int s = 0; s < KSTEPS; ++s)
           mma_f16(tmem, umma_desc(a_base + s * 2 * CHUNK_STRIDE, CHUNK_STRIDE, 128),
                   umma_desc(b_base + s * 2 * CHUNK_STRIDE, CHUNK_STRIDE, 128), s > 0);
         mma_commit(bar);
       }
+      // prefetch the next row while the tensor core works
+      if (t + 1 < T)
+        load_x((t + 1 < T - d) ? a.init32 + (t + 1) * 16 : a.rows32 + (off + (T - 2 - t)) * 16, x);
       mbar_wait(bar, phase);
       phase ^= 1u;
       fence_after();
       float acc = 0.0f;
+      float* prow = (a.record_prefix && r == 0) ? a.pre + (int64_t)(t + 1) * PRE_STRIDE : nullptr;
 #pragma unroll
       for (int g8 = 0; g8 < 4; ++g8) {
-        float zi[8], zf[8], zg[8], zo[8];
-        tmem_ld8(lane_addr + 0 * 32 + g8 * 8, zi);
-        tmem_ld8(lane_addr + 1 * 32 + g8 * 8, zf);
-        tmem_ld8(lane_addr + 2 * 32 + g8 * 8, zg);
-        tmem_ld8(lane_addr + 3 * 32 + g8 * 8, zo);
+        float ui[8], uf[8], vg[8], uo[8];
+        tmem_ld8(lane_addr + 0 * 32 + g8 * 8, ui);
+        tmem_ld8(lane_addr + 1 * 32 + g8 * 8, uf);
+        tmem_ld8(lane_addr + 2 * 32 + g8 * 8, vg);
+        tmem_ld8(lane_addr + 3 * 32 + g8 * 8, uo);
         tmem_wait_ld();
+        float h8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int j = g8 * 8 + u;
-          const float gi = sig_f(zi[u] + bias[j]);
-          const float gf = sig_f(zf[u] + bias[32 + j]);
-          const float gg = tanh_f(zg[u] + bias[64 + j]);
-          const float go = sig_f(zo[u] + bias[96 + j]);
+          const float gi = sig_u(ui[u]);
+          const float gf = sig_u(uf[u]);
+          const float gg = tanh_v(vg[u]);
+          const float go = sig_u(uo[u]);
           c[j] = fmaf(gf, c[j], gi * gg);
-          h[j] = go * tanh_f(c[j]);
-          acc = fmaf(h[j], wout[j], acc);
+          h8[u] = go * tanh_v(c2 * c[j]);
+          acc = fmaf(h8[u], wout[j], acc);
+        }
+        // the UMMA that read A has completed (mbarrier), so h can go straight in
+        put_h8(A, r, g8, h8);
+        if (prow) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            prow[g8 * 8 + u] = h8[u];
+            prow[32 + g8 * 8 + u] = c[g8 * 8 + u];
+          }
         }
       }
       raw = fadd(raw, (double)acc);
-      fence_before();
-      put_h(A, r, h);
+      if (prow) *reinterpret_cast<double*>(prow + 64) = raw;
+      fence_before();  // TMEM reads complete before the next UMMA overwrites D
     }
-    if (a.record_prefix) {
-      if (r == 0) {
-        float* p = a.pre + (int64_t)T * PRE_STRIDE;
-        for (int j = 0; j < 32; ++j) {
-          p[j] = h[j];
-          p[32 + j] = c[j];
-        }
-        *reinterpret_cast<double*>(p + 64) = raw;
-      }
-    } else if (valid) {
-      a.out[st] = exp(fadd(raw, a.target_scale));
-    }
-    __syncthreads();
+    if (!a.record_prefix && valid) a.out[st] = exp(fadd(raw, a.target_scale));
+    wg_sync(wg);
   }
   fence_before();
   __syncthreads();
   fence_after();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(NWG * 128)
+                 : "memory");
+}
+
+// Prefix position 0 (h = c = 0, raw = T * b_out) for the record pass.
+__global__ void k_prefix0(float* pre, int T, double b_out) {
+  const int j = threadIdx.x;
+  if (j < 64) pre[j] = 0.0f;
+  if (j == 0) *reinterpret_cast<double*>(pre + 64) = fmul((double)T, b_out);
 }
 
 // --------------------------------------------- featurize -> fp32 rows
@@ -329,9 +368,16 @@ __global__ void k_rows32(const double* __restrict__ rows64, int64_t n_words, flo
 }
 
 // --------------------------------------------- depth bucketing (counting sort)
-__global__ void k_depth_hist(const int64_t* __restrict__ offsets, int64_t n, int* __restrict__ hist) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(hist + (int)(offsets[i + 1] - offsets[i]), 1);
+// Block-local histogram in shared memory, then one global atomic per bin.
+__global__ void k_depth_hist(const int64_t* __restrict__ offsets, int64_t n, int T, int* __restrict__ hist) {
+  extern __shared__ int sh[];
+  for (int i = threadIdx.x; i <= T; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(sh + (int)(offsets[i + 1] - offsets[i]), 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= T; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
 // descending depth: cursor[d] = number of states with depth > d
@@ -345,24 +391,47 @@ __global__ void k_depth_scan(const int* __restrict__ hist, int T, int* __restric
   }
 }
 
+// Warp-aggregated scatter: one atomic per (warp, depth) group.
 __global__ void k_depth_scatter(const int64_t* __restrict__ offsets, int64_t n, int* __restrict__ cursor,
                                 int* __restrict__ perm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int d = (int)(offsets[i + 1] - offsets[i]);
-    perm[atomicAdd(cursor + d, 1)] = (int)i;
-  }
+  const bool ok = i < n;
+  const int d = ok ? (int)(offsets[i + 1] - offsets[i]) : -1;
+  const unsigned act = __ballot_sync(0xffffffffu, ok);
+  if (!ok) return;
+  const unsigned peers = __match_any_sync(act, d);
+  const int leader = __ffs(peers) - 1;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(cursor + d, __popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  perm[base + __popc(peers & ((1u << lane) - 1))] = (int)i;
 }
 
 // --------------------------------------------- host: weight image
 // B'[n][k] fp16 in the canonical K-major no-swizzle layout:
 // chunk kc (8 K-elements), row-group n>>3, row n&7 -> kc*2048 + (n>>3)*128 + (n&7)*16.
+// Gate columns scaled by -log2(e) (i, f, o) or -2 log2(e) (g); rows 144/145
+// carry the scaled bias split hi/lo.
 inline void pack_weights(const double* Wx, const double* Wh, const double* b, const double* w,
-                         uint8_t* img /* TILE_BYTES + 160*4 */) {
+                         uint8_t* img /* TILE_BYTES + 32*4 */) {
+  const double L2E = 1.4426950408889634074;
+  memset(img, 0, TILE_BYTES + 32 * 4);
   for (int n = 0; n < GN; ++n) {
+    const double scale = (n >= 64 && n < 96) ? -2.0 * L2E : -L2E;
     for (int k = 0; k < KP; ++k) {
-      const int seg = k / KA, kk = k % KA;
-      const double wv = kk < 16 ? Wx[kk * GN + n] : Wh[(kk - 16) * GN + n];
+      double wv;
+      int seg;
+      if (k < 3 * KA) {
+        seg = k / KA;
+        const int kk = k % KA;
+        wv = scale * (kk < 16 ? Wx[kk * GN + n] : Wh[(kk - 16) * GN + n]);
+      } else if (k == 3 * KA || k == 3 * KA + 1) {
+        seg = k == 3 * KA ? 0 : 2;  // b_hi, b_lo
+        wv = scale * b[n];
+      } else {
+        continue;
+      }
       const __half whi = __double2half(wv);
       const __half wlo = __double2half(wv - (double)__half2float(whi));
       const __half v = seg == 2 ? wlo : whi;
@@ -370,9 +439,8 @@ inline void pack_weights(const double* Wx, const double* Wh, const double* b, co
       memcpy(img + kc * CHUNK_STRIDE + (n >> 3) * 128 + (n & 7) * 16 + e * 2, &v, 2);
     }
   }
-  float* fb = reinterpret_cast<float*>(img + TILE_BYTES);
-  for (int j = 0; j < GN; ++j) fb[j] = (float)b[j];
-  for (int j = 0; j < 32; ++j) fb[GN + j] = (float)w[j];
+  float* fw = reinterpret_cast<float*>(img + TILE_BYTES);
+  for (int j = 0; j < 32; ++j) fw[j] = (float)w[j];
 }
 
 }  // namespace tc

@@ -33,6 +33,8 @@ extern "C" int core_featurize(const int64_t* desc, int64_t n_words, const ts_dec
         sd.cwindow[e][k] = w[38 + 4 * e + k];
       }
     sd.slot = (int)w[46];
+    sd.dp = make_divisor(sd.domain_points);
+    sd.io = make_divisor(1 + sd.i_in_bytes + sd.i_out_bytes);
   }
   for (int64_t i = 0; i < n; ++i) {
     double* o = out + i * T * 16;
@@ -49,8 +51,9 @@ extern "C" int core_featurize(const int64_t* desc, int64_t n_words, const ts_dec
       const StageDesc* cs = dec.anchor >= 0 ? &P.st[sd.consumer] : nullptr;
       const Nest* cn = dec.anchor >= 0 ? &slots[cs->slot] : nullptr;
       Nest nn;
-      int rc = build_nest(sd, cs, cn, dec, nn);
-      if (!rc) rc = acquired_features(sd, nn, dec, o + s * 16 + 8);
+      int64_t pe[TS_MAX_PURE];
+      int rc = build_nest(sd, cs, cn, dec, nn, pe);
+      if (!rc) rc = acquired_features(sd, nn, pe, dec, o + s * 16 + 8);
       if (rc) return rc;
       if (sd.slot >= 0) slots[sd.slot] = nn;
     }
@@ -63,7 +66,7 @@ extern "C" double core_log2(double x) { return glibc_log2(x); }
 extern "C" double core_div(const uint64_t* n4, uint64_t d) {
   u256 a;
   for (int i = 0; i < 4; ++i) a.w[i] = n4[i];
-  return u256_div_u64_to_double(a, d);
+  return u256_div_to_double(a, make_divisor(d));
 }
 
 extern "C" double core_to_double(const uint64_t* n4) {
