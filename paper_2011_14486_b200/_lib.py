@@ -17,7 +17,8 @@ import numpy as np
 
 from .errors import IllegalActionError, PipelineError
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "libtensched_b200.so"
+LIB_PATH = pathlib.Path(os.environ.get(
+    "TS_LIB", pathlib.Path(__file__).resolve().parent / "libtensched_b200.so"))
 
 TS_OK = 0
 TS_ERR_ILLEGAL = 4

@@ -581,7 +581,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
-          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
+          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
       TS_LAUNCHED();
     }
@@ -620,7 +620,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
-          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_raw.as<double>(),
+          P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>());
       TS_LAUNCHED();
     }

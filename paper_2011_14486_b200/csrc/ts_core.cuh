@@ -82,12 +82,17 @@ TS_HD uint64_t as_u64(double d) {
 
 // ------------------------------------------------------- glibc 2.39 log2
 #ifdef __CUDACC__
-__device__ __constant__ uint64_t d_log2_data[TS_LOG2_NDATA];
+// Global (not __constant__): the table index differs per lane, which the
+// constant cache would serialize; __ldg keeps it in L1.
+__device__ uint64_t d_log2_data[TS_LOG2_NDATA];
+#define TS_HD_NOINLINE __host__ __device__ __noinline__
+#else
+#define TS_HD_NOINLINE inline
 #endif
 
 TS_HD double log2_c(int i) {
 #ifdef __CUDA_ARCH__
-  return as_double(d_log2_data[i]);
+  return as_double(__ldg(reinterpret_cast<const unsigned long long*>(d_log2_data) + i));
 #else
   return as_double(ts_log2_data_bits[i]);
 #endif
@@ -97,10 +102,14 @@ TS_HD double log2_c(int i) {
 // the x86-64 FMA ifunc variant (libm 0x79f90).  The
 // contraction pattern below was read off that binary; all other ops are
 // single IEEE operations.  Not correctly rounded - bit-compatibility with
-// the reference's math.log2 is the point.
+// the reference's math.log2 is the point.  Powers of two short-circuit to
+// their exponent: glibc returns them exactly (checked over all 2098 normal
+// and subnormal powers, tests/test_host.py).
 TS_HD double glibc_log2(double x) {
   const uint64_t ix0 = as_u64(x);
   uint64_t ix = ix0;
+  if ((ix & 0x000FFFFFFFFFFFFFull) == 0 && ix - 0x0010000000000000ull < 0x7FE0000000000000ull)
+    return (double)((int)(ix >> 52) - 1023);
   // |x - 1| small: dedicated polynomial (wrapping unsigned compare).
   if (ix - 0x3feea4af00000000ull <= 0x210a9ffffffffull) {
     if (ix == 0x3ff0000000000000ull) return 0.0;
@@ -259,7 +268,7 @@ TS_HD double make_double(uint64_t mant, int e2) {
 
 // Round q + f (0 <= f < 1, f > 0 iff sticky) to 53 bits half-even, times
 // 2^e2.  Callers guarantee q has >= 55 bits whenever sticky is set.
-TS_HD double round_u256(const u256& q, bool sticky, int e2) {
+TS_HD_NOINLINE double round_u256(const u256& q, bool sticky, int e2) {
   const int bl = u256_bitlen(q);
   if (bl == 0) return 0.0;
   if (bl <= 53) {
@@ -333,9 +342,7 @@ TS_HD u256 u256_div(const u256& a, const Divisor& D, bool& inexact) {
 }
 
 // CPython int/int true division (long_true_divide): correctly rounded n/d.
-TS_HD double u256_div_to_double(const u256& n, const Divisor& D) {
-  if (u256_small(n) && n.w[0] <= (1ull << 53) && D.d <= (1ull << 53))
-    return fdiv(u64_to_double(n.w[0]), u64_to_double(D.d));  // both exact: IEEE division
+TS_HD_NOINLINE double u256_div_to_double_slow(const u256& n, const Divisor& D) {
   const int a = u256_bitlen(n);
   if (a == 0) return 0.0;
   const int b = 64 - clz64(D.d);
@@ -345,6 +352,12 @@ TS_HD double u256_div_to_double(const u256& n, const Divisor& D) {
   bool inexact;
   const u256 q = u256_div(N, D, inexact);
   return round_u256(q, inexact, -k);
+}
+
+TS_HD double u256_div_to_double(const u256& n, const Divisor& D) {
+  if (u256_small(n) && n.w[0] <= (1ull << 53) && D.d <= (1ull << 53))
+    return fdiv(u64_to_double(n.w[0]), u64_to_double(D.d));  // both exact: IEEE division
+  return u256_div_to_double_slow(n, D);
 }
 
 // ------------------------------------------------------------ descriptor

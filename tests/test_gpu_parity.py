@@ -168,3 +168,23 @@ def test_fast_mode_large_batch_matches_exact(gpu_ctx, v0):
         out[mode] = o.cpu().numpy()
     assert np.all(out[MODE_EXACT] > 0)
     np.testing.assert_allclose(out[MODE_FAST], out[MODE_EXACT], rtol=FAST_RTOL, atol=0)
+
+
+def test_reference_greedy_with_gpu_v_callable(greedy_golden, v0_path):
+    """INTEGRATION.md level 1: the unmodified reference's greedy_schedule
+    driven by the device V-callable, on the reference's own objects."""
+    import pathlib
+    import sys
+    ref = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
+    if not (ref / "tensched").exists():
+        pytest.skip("oracle/_ref (the built reference) is not present")
+    sys.path.insert(0, str(ref))
+    from tensched.pipeline_ir import parse_pipeline as ref_parse
+    from tensched.search import greedy_schedule as ref_greedy
+    from tensched.value_model import load as ref_load
+    from paper_2011_14486_b200.search import model_value as gpu_model_value
+    params = ref_load(v0_path)
+    for key in ("ref:pipelines/toys/t5_diamond.pl", "ref:pipelines/deep/p12_deep.pl"):
+        g = greedy_golden[key]
+        s, visited = ref_greedy(ref_parse(g["text"]), gpu_model_value(params))
+        assert [d.render() for d in s.decisions] == g["schedule"] and visited == g["visited"]

@@ -140,3 +140,12 @@ def test_native_core_features_bit_exact(state_sets, native_core):
                                             out.ctypes.data)
             assert rc == 0
             assert np.array_equal(bits(out), bits(z["features"][idxs])), name
+
+
+def test_glibc_log2_exact_on_powers_of_two(native_core):
+    """The device log2 short-circuits powers of two to their exponent; glibc
+    returns them exactly (all normal and subnormal powers)."""
+    for k in range(-1074, 1024):
+        x = 2.0 ** k
+        assert math.log2(x) == k
+        assert native_core.core_log2(x) == k
