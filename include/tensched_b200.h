@@ -147,6 +147,24 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
 int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
                               ts_decision* d_records, int64_t* d_offsets, int64_t* n_records);
 
+/* ---- V training (value_model.train / gradients, value_model.py:182-293;
+ * lstm_forward_cached / lstm_backward, _recurrent_np.py:38-96).
+ * The dataset is uploaded once as normalized matrices X[N][Tmax][16] with
+ * per-entry lengths and log targets; parameters are a flat f64 vector
+ * [Wx 16x4H | Wh Hx4H | b 4H | w H | b_out] resident on the device. */
+int ts_train_load(ts_ctx* ctx, const double* X, const int32_t* Tlen, const double* logt, int64_t N,
+                  int Tmax, int hidden);
+int ts_train_set_params(ts_ctx* ctx, const double* flat, int64_t n);
+int ts_train_get_params(ts_ctx* ctx, double* flat, int64_t n);
+/* gradient of the loss over idx[0..B) of a minibatch of global size n_total
+ * into d_grad (device pointer; null = context buffer); raw_out optional. */
+int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, double target_scale,
+                   double* d_grad, double* raw_out);
+/* _clip (global L2 incl. b_out) + SGD with the gradient in d_grad. */
+int ts_train_apply(ts_ctx* ctx, const double* d_grad, double lr, double clip_norm, double* norm_out);
+/* raw scores of dataset entries idx[0..n) (for _eval_split). */
+int ts_train_forward(ts_ctx* ctx, const int32_t* idx, int64_t n, double* raw_out);
+
 /* Synchronize the context stream; cudaStream_t of the context (as void*). */
 int ts_sync(ts_ctx* ctx);
 void* ts_stream(ts_ctx* ctx);

@@ -360,3 +360,56 @@ def random_partial(P: Pipe, seed: int):
         c = candidates(P, decisions)
         decisions.append(c[rng.randrange(len(c))])
     return decisions
+
+
+# ------------------------------------------------------------------ training
+def _sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def gradients(params, X_list, logt, n_total=None):
+    """value_model.gradients (value_model.py:182-210) for a list of
+    normalized matrices grouped by length (ascending), via the numpy BPTT of
+    _recurrent_np.py:38-96.  Returns the flat [Wx|Wh|b|w|b_out] gradient."""
+    Wx, Wh, b, w, b_out = params["Wx"], params["Wh"], params["b"], params["w"], params["b_out"]
+    H = len(w)
+    n = len(X_list) if n_total is None else n_total
+    gWx, gWh, gb, gw, gbo = np.zeros_like(Wx), np.zeros_like(Wh), np.zeros(4 * H), np.zeros(H), 0.0
+    groups = {}
+    for m, lt in zip(X_list, logt):
+        groups.setdefault(m.shape[0], []).append((m, lt))
+    for T, items in sorted(groups.items()):
+        X = np.stack([m for m, _ in items])
+        lt = np.array([v for _, v in items])
+        B = X.shape[0]
+        h, c = np.zeros((B, H)), np.zeros((B, H))
+        raw = np.full(B, T * b_out)
+        cache = []
+        for t in range(T):
+            z = X[:, t, :] @ Wx + h @ Wh + b
+            i, f = _sigmoid(z[:, :H]), _sigmoid(z[:, H:2 * H])
+            g, o = np.tanh(z[:, 2 * H:3 * H]), _sigmoid(z[:, 3 * H:])
+            c_prev, h_prev = c, h
+            c = f * c + i * g
+            tc = np.tanh(c)
+            h = o * tc
+            raw += h @ w
+            cache.append((i, f, g, o, c_prev, h_prev, tc, h))
+        d_raw = 2.0 * (raw + params["target_scale"] - lt) / n
+        gbo += T * d_raw.sum()
+        dh_next, dc_next = np.zeros((B, H)), np.zeros((B, H))
+        for t in range(T - 1, -1, -1):
+            i, f, g, o, c_prev, h_prev, tc, h = cache[t]
+            gw += h.T @ d_raw
+            dh = w[None, :] * d_raw[:, None] + dh_next
+            do = dh * tc
+            dc = dc_next + dh * o * (1.0 - tc * tc)
+            di, df, dg = dc * g, dc * c_prev, dc * i
+            dc_next = dc * f
+            dz = np.concatenate([di * i * (1 - i), df * f * (1 - f), dg * (1 - g * g),
+                                 do * o * (1 - o)], axis=1)
+            gWx += X[:, t, :].T @ dz
+            gWh += h_prev.T @ dz
+            gb += dz.sum(axis=0)
+            dh_next = dz @ Wh.T
+    return np.concatenate([gWx.ravel(), gWh.ravel(), gb, gw, [gbo]])

@@ -78,6 +78,12 @@ def load_library():
             "ts_launch_count": ([vp], i64),
             "ts_set_timing": ([vp, i32], i32),
             "ts_kernel_times": ([vp, vp, vp, i32], i32),
+            "ts_train_load": ([vp, vp, vp, vp, i64, i32, i32], i32),
+            "ts_train_set_params": ([vp, vp, i64], i32),
+            "ts_train_get_params": ([vp, vp, i64], i32),
+            "ts_train_grads": ([vp, vp, i64, i64, f64, vp, vp], i32),
+            "ts_train_apply": ([vp, vp, f64, f64, vp], i32),
+            "ts_train_forward": ([vp, vp, i64, vp], i32),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(lib, name)

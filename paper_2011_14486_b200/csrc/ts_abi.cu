@@ -21,6 +21,7 @@
 #include "ts_core.cuh"
 #include "ts_kernels.cuh"
 #include "ts_lstm_tc.cuh"
+#include "ts_train.cuh"
 
 using namespace ts;
 
@@ -112,6 +113,10 @@ struct ts_ctx {
   std::vector<cudaEvent_t> event_pool;
   double kms[TS_KCLASSES] = {0};
   int64_t kcount[TS_KCLASSES] = {0};
+  // V training (ts_train_*)
+  int tr_H = 0, tr_Tmax = 0;
+  int64_t tr_N = 0;
+  DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm;
 };
 
 namespace {
@@ -914,6 +919,140 @@ int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int6
   TS_LAUNCHED();
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
   *n_records = ho[n_states];
+  return TS_OK;
+}
+
+// ------------------------------------------------------------------ training
+int ts_train_load(ts_ctx* ctx, const double* X, const int32_t* Tlen, const double* logt, int64_t N, int Tmax,
+                  int hidden) {
+  if (!ctx || !X || !Tlen || !logt || N < 1 || Tmax < 1) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (hidden < 1 || hidden > 32) return fail(ctx, TS_ERR_ARG, "hidden size must be in 1..32");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->tr_H = hidden;
+  ctx->tr_Tmax = Tmax;
+  ctx->tr_N = N;
+  TS_CUDA(ctx->tr_X.reserve(sizeof(double) * N * Tmax * F));
+  TS_CUDA(ctx->tr_T.reserve(sizeof(int32_t) * N));
+  TS_CUDA(ctx->tr_logt.reserve(sizeof(double) * N));
+  TS_CUDA(cudaMemcpy(ctx->tr_X.p, X, sizeof(double) * N * Tmax * F, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->tr_T.p, Tlen, sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpy(ctx->tr_logt.p, logt, sizeof(double) * N, cudaMemcpyHostToDevice));
+  const tr::Layout L(hidden);
+  TS_CUDA(ctx->tr_P.reserve(sizeof(double) * L.n));
+  TS_CUDA(ctx->tr_grad.reserve(sizeof(double) * L.n));
+  TS_CUDA(ctx->tr_norm.reserve(sizeof(double)));
+  return TS_OK;
+}
+
+int ts_train_set_params(ts_ctx* ctx, const double* flat, int64_t n) {
+  if (!ctx || !flat) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  const tr::Layout L(ctx->tr_H);
+  if (!ctx->tr_H || n != L.n) return fail(ctx, TS_ERR_ARG, "parameter vector size");
+  TS_CUDA(cudaMemcpyAsync(ctx->tr_P.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
+int ts_train_get_params(ts_ctx* ctx, double* flat, int64_t n) {
+  if (!ctx || !flat) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  const tr::Layout L(ctx->tr_H);
+  if (!ctx->tr_H || n != L.n) return fail(ctx, TS_ERR_ARG, "parameter vector size");
+  TS_CUDA(cudaMemcpyAsync(flat, ctx->tr_P.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
+static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs& a) {
+  TS_CUDA(ctx->tr_batch.reserve(sizeof(int32_t) * B));
+  TS_CUDA(ctx->tr_raw.reserve(sizeof(double) * B));
+  TS_CUDA(ctx->tr_draw.reserve(sizeof(double) * B));
+  TS_CUDA(cudaMemcpyAsync(ctx->tr_batch.p, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, ctx->stream));
+  a.X = ctx->tr_X.as<double>();
+  a.Tlen = ctx->tr_T.as<int>();
+  a.logt = ctx->tr_logt.as<double>();
+  a.batch = ctx->tr_batch.as<int>();
+  a.P = ctx->tr_P.as<double>();
+  a.cache = nullptr;
+  a.dz = nullptr;
+  a.draw = ctx->tr_draw.as<double>();
+  a.raw = ctx->tr_raw.as<double>();
+  a.B = (int)B;
+  a.Tmax = ctx->tr_Tmax;
+  a.H = ctx->tr_H;
+  a.target_scale = 0.0;
+  a.n_total = 1.0;
+  return TS_OK;
+}
+
+// Gradient of the loss over this rank's part of a minibatch whose global size
+// is n_total (d_raw divides by it); written to d_grad (device pointer, or the
+// context's buffer when null).  Data-parallel callers all-reduce d_grad.
+int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, double target_scale,
+                   double* d_grad, double* raw_out) {
+  if (!ctx || !idx || B < 0 || n_total < 1) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (!ctx->tr_H) return fail(ctx, TS_ERR_STATE, "no training data loaded");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const tr::Layout L(ctx->tr_H);
+  double* grad = d_grad ? d_grad : ctx->tr_grad.as<double>();
+  if (B == 0) {
+    TS_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * L.n, ctx->stream));
+    return TS_OK;
+  }
+  tr::TrainArgs a;
+  int rc = train_args(ctx, idx, B, a);
+  if (rc) return rc;
+  TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
+  TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * B * ctx->tr_Tmax * L.G));
+  a.cache = ctx->tr_cache.as<double>();
+  a.dz = ctx->tr_dz.as<double>();
+  a.target_scale = target_scale;
+  a.n_total = (double)n_total;
+  tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
+  TS_LAUNCHED();
+  tr::k_train_wgrad<<<(L.n + 255) / 256, 256, 0, ctx->stream>>>(a, grad);
+  TS_LAUNCHED();
+  if (raw_out) {
+    TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return TS_OK;
+}
+
+// _clip + SGD step with the gradient in d_grad (or the context buffer).
+int ts_train_apply(ts_ctx* ctx, const double* d_grad, double lr, double clip_norm, double* norm_out) {
+  if (!ctx) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (!ctx->tr_H) return fail(ctx, TS_ERR_STATE, "no training data loaded");
+  const tr::Layout L(ctx->tr_H);
+  const double* grad = d_grad ? d_grad : ctx->tr_grad.as<double>();
+  tr::k_train_apply<<<1, 1024, 0, ctx->stream>>>(ctx->tr_P.as<double>(), grad, L.n, lr, clip_norm,
+                                                 ctx->tr_norm.as<double>());
+  TS_LAUNCHED();
+  if (norm_out) {
+    TS_CUDA(cudaMemcpyAsync(norm_out, ctx->tr_norm.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return TS_OK;
+}
+
+// raw scores of dataset entries idx[0..n) under the current training params.
+int ts_train_forward(ts_ctx* ctx, const int32_t* idx, int64_t n, double* raw_out) {
+  if (!ctx || !idx || !raw_out || n < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (!ctx->tr_H) return fail(ctx, TS_ERR_STATE, "no training data loaded");
+  if (n == 0) return TS_OK;
+  tr::TrainArgs a;
+  int rc = train_args(ctx, idx, n, a);
+  if (rc) return rc;
+  tr::k_train_fwd<<<(unsigned)((n * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
+  TS_LAUNCHED();
+  TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   return TS_OK;
 }
 

@@ -146,3 +146,29 @@ def load(path) -> ValueModelParams:
         raise
     except Exception as e:
         raise CheckpointError(f"corrupt checkpoint: {e}") from None
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """value_model.py:74-88 (library defaults)."""
+
+    learning_rate: float = 1e-2
+    epochs: int = 200
+    batch_size: int = 32
+    seed: int = 0
+    clip_norm: float = 5.0
+    holdout_fraction: float = 0.2
+    patience: int = 20
+
+    def __post_init__(self):
+        if not 0 < self.holdout_fraction < 1:
+            raise PipelineError("holdout fraction must be in (0, 1)")
+        if min(self.learning_rate, self.epochs, self.batch_size, self.clip_norm,
+               self.patience) <= 0:
+            raise PipelineError("train config values must be positive")
+
+
+def train(params, dataset, cfg, device=None, dist=None):
+    """value_model.train on the device (see trainer.py)."""
+    from .trainer import train as _train
+    return _train(params, dataset, cfg, device=device, dist=dist)

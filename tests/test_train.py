@@ -1,0 +1,138 @@
+"""V training: device gradients against the oracle's numpy BPTT, the full
+device training run against the reference-trained v0 (same data, same
+PCG64 trajectory), and the data-parallel sharding/all-reduce logic on CPU
+(gloo, world size 2)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2011_14486_b200 import pipeline_ir as pi
+from paper_2011_14486_b200 import schedule_space as ss
+from paper_2011_14486_b200.trainer import shard
+
+
+def _dataset(golden):
+    g = json.loads((golden / "train_v0.json").read_text())
+    pipes = {n: pi.parse_pipeline(t) for n, t in g["pipelines"].items()}
+    states = []
+    for k in g["keys"]:
+        states.append(ss.state_from_key(pipes[k.split("/", 1)[0]], k))
+    targets = [float.fromhex(t) for t in g["targets"]]
+    return g, list(zip(states, targets))
+
+
+# ---------------------------------------------------------------- CPU (gloo)
+def _dp_worker(rank, world, port, X, logt, params, batch, q):
+    import pathlib
+    import sys
+    root = pathlib.Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "oracle"))
+    import torch
+    import torch.distributed as dist
+    import oracle as Or
+    from paper_2011_14486_b200.trainer import shard as sh
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    part = sh(batch, rank, world)
+    g = Or.gradients(params, [X[i] for i in part], logt[part], n_total=len(batch))
+    t = torch.from_numpy(g.copy())
+    dist.all_reduce(t)
+    q.put((rank, t.numpy()))
+    dist.destroy_process_group()
+
+
+def test_data_parallel_gradient_equals_single_process(v0_path):
+    """Shards of a length-sorted global minibatch, d_raw divided by the
+    global size, summed by all-reduce (gloo, 2 ranks) == the single-process
+    gradient - the host logic of trainer.train(dist=...)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    params = O.load_checkpoint(v0_path)
+    rng = np.random.default_rng(0)
+    T = np.array([2, 2, 3, 3, 3, 2, 3, 2, 3, 3, 2])
+    X = [rng.normal(size=(t, 16)) for t in T]
+    logt = rng.normal(3.0, 1.0, size=len(T))
+    batch = np.argsort(T, kind="stable")
+    full = O.gradients(params, [X[i] for i in batch], logt[batch])
+    world = 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dp_worker, args=(r, world, port, X, logt, params, batch, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        np.testing.assert_allclose(res[r], full, rtol=1e-12, atol=1e-15)
+    np.testing.assert_array_equal(res[0], res[1])
+
+
+def test_shard_covers_batch():
+    b = np.arange(17)
+    parts = [shard(b, r, 4) for r in range(4)]
+    assert np.array_equal(np.concatenate(parts), b)
+    assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+# ---------------------------------------------------------------- GPU
+@pytest.mark.gpu
+def test_device_gradients_match_oracle(golden, v0_path):
+    from paper_2011_14486_b200 import _lib
+    from paper_2011_14486_b200.featurizer import featurize_states, normalize
+    from paper_2011_14486_b200.trainer import DeviceGradients, flat_params
+    from paper_2011_14486_b200.value_model import load
+    g, data = _dataset(golden)
+    params = load(v0_path)
+    oparams = O.load_checkpoint(v0_path)
+    mats = featurize_states([s for s, _ in data[:64]])
+    Xn = [normalize(params.normalizer, m) for m in mats]
+    T = np.array([m.shape[0] for m in mats], dtype=np.int32)
+    X = np.zeros((len(mats), T.max(), 16))
+    for i, m in enumerate(Xn):
+        X[i, : len(m)] = m
+    logt = np.log([t for _, t in data[:64]])
+    dev = DeviceGradients(_lib.context(0), X, T, logt, params.hidden)
+    dev.set_params(flat_params(params))
+    batch = np.argsort(T[:16], kind="stable")
+    dev.grads(batch, len(batch), params.target_scale)
+    import torch
+    gbuf = torch.zeros(dev.n_params, dtype=torch.float64, device="cuda")
+    dev.grads(batch, len(batch), params.target_scale, gbuf.data_ptr())
+    dev.sync()
+    want = O.gradients(oparams, [Xn[i] for i in batch], logt[batch])
+    np.testing.assert_allclose(gbuf.cpu().numpy(), want, rtol=1e-9, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_device_training_reproduces_reference_v0(golden, v0_path):
+    """`tensched train <train assets> --rounds 0 --seed 0` on the device:
+    same PCG64 split/permutations, final V within 1e-4 of the reference's
+    v0 on the dataset, holdout R^2 equal to 4 decimals."""
+    from paper_2011_14486_b200.trainer import train
+    from paper_2011_14486_b200.value_model import TrainConfig, init_params, load, predict_states
+    g, data = _dataset(golden)
+    c = g["config"]
+    cfg = TrainConfig(c["learning_rate"], c["epochs"], c["batch_size"], c["seed"], c["clip_norm"],
+                      c["holdout_fraction"], c["patience"])
+    params, metrics = train(init_params(c["seed"], c["hidden"]), data, cfg)
+    ref = load(v0_path)
+    assert params.target_scale == ref.target_scale
+    assert np.array_equal(params.normalizer.mean, ref.normalizer.mean)
+    assert np.array_equal(params.normalizer.std, ref.normalizer.std)
+    states = [s for s, _ in data]
+    v_dev = predict_states(params, states)
+    v_ref = predict_states(ref, states)
+    rel = np.abs(v_dev / v_ref - 1)
+    assert rel.max() <= 1e-4, rel.max()
+    assert abs(metrics["holdout_r2"] - g["metrics"]["holdout_r2"]) < 5e-5
