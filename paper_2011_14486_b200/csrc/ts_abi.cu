@@ -87,7 +87,8 @@ struct PipelineSlot {
 
 struct ts_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;       // compute
+  cudaStream_t copy_stream = nullptr;  // host<->device transfers of ts_score_states
   std::string err;
   std::vector<std::unique_ptr<PipelineSlot>> pipes;
   // parameters
@@ -328,6 +329,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
   ctx->sm_count = prop.multiProcessorCount;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess)
     e = cudaMemcpyToSymbol(d_log2_data, ts_log2_data_bits, sizeof(uint64_t) * TS_LOG2_NDATA);
   if (e == cudaSuccess) e = ctx->status.reserve(sizeof(int));
@@ -368,10 +370,13 @@ void ts_ctx_destroy(ts_ctx* ctx) {
   }
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
   ctx->pipes.clear();
-  cudaStream_t s = ctx->stream;
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  cudaStream_t s = ctx->stream, c = ctx->copy_stream;
   delete ctx;
   if (s) cudaStreamDestroy(s);
+  if (c) cudaStreamDestroy(c);
 }
 
 int ts_set_timing(ts_ctx* ctx, int on) {
@@ -666,16 +671,44 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, co
   TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n_rec > 0 ? n_rec : 1)));
   TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
   TS_CUDA(ctx->out.reserve(sizeof(double) * n_states));
-  if (n_rec)
-    TS_CUDA(cudaMemcpyAsync(ctx->records.p, records, sizeof(ts_decision) * n_rec, cudaMemcpyHostToDevice,
-                            ctx->stream));
-  TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n_states + 1),
-                          cudaMemcpyHostToDevice, ctx->stream));
-  int rc = score_device(ctx, P, ctx->records.as<ts_decision>(), ctx->offsets.as<int64_t>(), n_states,
-                        n_rec, mode, ctx->out.as<double>());
+  int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
-  TS_CUDA(cudaMemcpyAsync(out_v, ctx->out.p, sizeof(double) * n_states, cudaMemcpyDeviceToHost,
-                          ctx->stream));
+  if (mode == TS_MODE_FAST) {
+    rc = ensure_fast_prefix(ctx, P);
+    if (rc) return rc;
+  }
+  // Pipelined host path: every chunk's records are queued H2D on the copy
+  // stream up front; the compute stream scores chunk k as soon as its copy
+  // event fires (while chunk k+1 is still in flight) and returns its V D2H.
+  // Offsets stay absolute, so every chunk indexes the one device records array.
+  int64_t chunk = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 18, (n_states + 7) / 8));
+  if (chunk > n_states) chunk = n_states;
+  const int64_t n_chunks = (n_states + chunk - 1) / chunk;
+  TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n_states + 1), cudaMemcpyHostToDevice,
+                          ctx->copy_stream));
+  ts_decision* d_rec = ctx->records.as<ts_decision>();
+  std::vector<cudaEvent_t> ev;
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int64_t s0 = k * chunk, s1 = std::min(n_states, s0 + chunk);
+    const int64_t r0 = offsets[s0], r1 = offsets[s1];
+    if (r1 > r0)
+      TS_CUDA(cudaMemcpyAsync(d_rec + r0, records + r0, sizeof(ts_decision) * (r1 - r0), cudaMemcpyHostToDevice,
+                              ctx->copy_stream));
+    cudaEvent_t in = take_event(ctx);
+    ev.push_back(in);
+    TS_CUDA(cudaEventRecord(in, ctx->copy_stream));
+  }
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int64_t s0 = k * chunk, s1 = std::min(n_states, s0 + chunk);
+    TS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
+    rc = score_device(ctx, P, d_rec, ctx->offsets.as<int64_t>() + s0, s1 - s0, n_rec, mode,
+                      ctx->out.as<double>() + s0);
+    if (rc) return rc;
+    TS_CUDA(cudaMemcpyAsync(out_v + s0, ctx->out.as<double>() + s0, sizeof(double) * (s1 - s0),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  for (auto e : ev) ctx->event_pool.push_back(e);
   return check_device_status(ctx);
 }
 
