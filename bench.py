@@ -301,22 +301,33 @@ def main():
     avg = {names[k]: times[k] / counts[k] for k in range(4) if counts[k]}
     dom = max(avg, key=lambda k: times[names.index(k)])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    # ncu --set full capture (profiles/r01_ncu.md): DRAM bytes per state of each
+    # kernel at 262,144 states, scaled to this launch
+    traffic_per_state = {"featurize": (100.080128e6 + 368.331776e6) / 262144,
+                         "lstm_fast": (309.275648e6 + 4.245760e6) / 262144}
+    row_bytes = 64 if mode == _lib.MODE_FAST else ROW_BYTES
     if dom == "featurize":
-        bytes_per_launch = n_records * (RECORD_BYTES + ROW_BYTES) + 8 * (M + 1)
+        bytes_per_launch = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
         achieved = bytes_per_launch / (avg[dom] / 1e3) / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
+        tr = traffic_per_state.get(dom)
         roof = {"kernel": "k_featurize_rows", "bound": "hbm", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                "algorithmic": "16 B record read + 128 B row written per scheduled stage"}
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": tr * M if tr and mode == _lib.MODE_FAST else None,
+                "bytes_per_launch": bytes_per_launch,
+                "algorithmic": f"16 B record read + {row_bytes} B row written per scheduled stage"}
     else:
         flops_per_launch = FLOPS_PER_STEP * timesteps
         achieved = flops_per_launch / (avg[dom] / 1e3) / 1e12
         peak = peaks.get("bf16_tflops", 1590.0)
+        tr = traffic_per_state.get(dom)
         roof = {"kernel": "k_lstm_tc" if dom == "lstm_fast" else "k_score_exact", "bound": "tensor",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None,
+                "traffic": tr * M if tr else None, "flops_per_launch": flops_per_launch,
                 "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
     roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
+    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU-bound (XU pipe 89% "
+                    "in ncu), k_featurize_rows is issue/divergence-bound (profiles/r01_ncu.md)")
 
     greedy = {}
     if rank == 0 and not args.no_greedy:

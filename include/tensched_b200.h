@@ -147,6 +147,21 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
 int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
                               ts_decision* d_records, int64_t* d_offsets, int64_t* n_records);
 
+/* Complete random schedules (search.random_schedule, search.py:136-142):
+ * schedule i uses SearchRng(seed0 + i); records at d_records[i*T .. i*T+T). */
+int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
+                                 ts_decision* d_records);
+
+/* cost_oracle.benchmark (cost_oracle.py:313-357) for complete schedules:
+ * total_millis as 4 little-endian u64 limbs per schedule.  cost_desc: per
+ * stage (topological order) flops_per_point, n_inputs, then 4 input slots of
+ * [producer stage (-1 = buffer), elem bytes, n_maps, 6 x (consumer dim,
+ * stride, window)]; machine: flop_cost, mem_byte_cost, cache_byte_cost,
+ * cache_size, cores, task_overhead. */
+int ts_benchmark(ts_ctx* ctx, int pipeline_id, const int64_t* cost_desc, int64_t n_words,
+                 const uint64_t* machine, const ts_decision* records, const int64_t* offsets, int64_t n,
+                 uint64_t* out_millis);
+
 /* ---- V training (value_model.train / gradients, value_model.py:182-293;
  * lstm_forward_cached / lstm_backward, _recurrent_np.py:38-96).
  * The dataset is uploaded once as normalized matrices X[N][Tmax][16] with

@@ -22,6 +22,7 @@
 #include "ts_kernels.cuh"
 #include "ts_lstm_tc.cuh"
 #include "ts_train.cuh"
+#include "ts_cost.cuh"
 
 using namespace ts;
 
@@ -923,6 +924,73 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   return TS_OK;
 }
 
+int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
+                                 ts_decision* d_records) {
+  if (!ctx || !d_records || n < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  TS_CUDA(ctx->tmp.reserve(sizeof(int) * (n > 0 ? n : 1)));
+  k_generate<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), seed0, n, d_records, ctx->tmp.as<int>(), ctx->status.as<int>(), 1);
+  TS_LAUNCHED();
+  return check_device_status(ctx);
+}
+
+int ts_benchmark(ts_ctx* ctx, int pipeline_id, const int64_t* cost_desc, int64_t n_words,
+                 const uint64_t* machine, const ts_decision* records, const int64_t* offsets, int64_t n,
+                 uint64_t* out_millis) {
+  if (!ctx || !cost_desc || !machine || !offsets || !out_millis || n < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n == 0) return TS_OK;
+  const int T = P->h->n_stages;
+  if (n_words != (int64_t)T * cost::WORDS_PER_STAGE) return fail(ctx, TS_ERR_ARG, "cost descriptor size");
+  auto C = std::make_unique<cost::CostDesc>();
+  for (int s = 0; s < T; ++s) {
+    const int64_t* w = cost_desc + (int64_t)s * cost::WORDS_PER_STAGE;
+    cost::StageCostDesc& sc = C->st[s];
+    sc.flops_per_point = (uint64_t)w[0];
+    sc.n_in = (int32_t)w[1];
+    if (sc.n_in < 0 || sc.n_in > cost::MAX_IN) return fail(ctx, TS_ERR_PIPELINE, "more than 4 inputs");
+    for (int e = 0; e < cost::MAX_IN; ++e) {
+      const int64_t* q = w + 2 + e * cost::WORDS_PER_IN;
+      cost::Edge& ed = sc.in[e];
+      ed.producer = (int32_t)q[0];
+      ed.elem = (int32_t)q[1];
+      ed.n_maps = (int32_t)q[2];
+      if (ed.n_maps < 0 || ed.n_maps > cost::MAX_MAPS) return fail(ctx, TS_ERR_PIPELINE, "more than 6 maps");
+      for (int k = 0; k < cost::MAX_MAPS; ++k) {
+        ed.cdim[k] = (int32_t)q[3 + 3 * k];
+        ed.stride[k] = q[4 + 3 * k];
+        ed.window[k] = q[5 + 3 * k];
+      }
+    }
+  }
+  cost::Machine m{machine[0], machine[1], machine[2], machine[3], machine[4], machine[5]};
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t n_rec = offsets[n];
+  TS_CUDA(ctx->tmp2.reserve(sizeof(cost::CostDesc)));
+  TS_CUDA(cudaMemcpyAsync(ctx->tmp2.p, C.get(), sizeof(cost::CostDesc), cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n_rec > 0 ? n_rec : 1)));
+  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n + 1)));
+  TS_CUDA(ctx->out.reserve(sizeof(uint64_t) * 4 * n));
+  TS_CUDA(ctx->tmp.reserve(sizeof(cost::StageRec) * n * T));
+  if (n_rec)
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, records, sizeof(ts_decision) * n_rec, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->offsets.p, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ctx->stream));
+  cost::k_benchmark<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), ctx->tmp2.as<cost::CostDesc>(), m, ctx->records.as<ts_decision>(),
+      ctx->offsets.as<int64_t>(), n, ctx->tmp.as<cost::StageRec>(), ctx->out.as<uint64_t>(),
+      ctx->status.as<int>());
+  TS_LAUNCHED();
+  TS_CUDA(cudaMemcpyAsync(out_millis, ctx->out.p, sizeof(uint64_t) * 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  return check_device_status(ctx);
+}
+
 int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
                               ts_decision* d_records, int64_t* d_offsets, int64_t* n_records) {
   if (!ctx || !d_records || !d_offsets || !n_records || n_states < 0) return TS_ERR_ARG;
@@ -935,7 +1003,7 @@ int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int6
   ts_decision* fixed = ctx->tmp.as<ts_decision>();
   int* depth = reinterpret_cast<int*>(fixed + n_states * T);
   k_generate<<<(unsigned)((n_states + 127) / 128), 128, 0, ctx->stream>>>(
-      P->d.as<PipelineDesc>(), seed0, n_states, fixed, depth, ctx->status.as<int>());
+      P->d.as<PipelineDesc>(), seed0, n_states, fixed, depth, ctx->status.as<int>(), 0);
   // (the generator keeps its nests in registers/local memory: untimed)
   TS_LAUNCHED();
   std::vector<int> hd(n_states);
