@@ -54,6 +54,9 @@ def parse_args():
     ap.add_argument("--cpu-states", type=int, default=1500, help="reference states per process")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-greedy", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-pairs", type=int, default=10_000_000, help="training pairs per GPU")
+    ap.add_argument("--train-batch", type=int, default=4096, help="per-GPU minibatch")
     return ap.parse_args()
 
 
@@ -181,6 +184,94 @@ def run_reference_arm(args):
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- V training
+def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
+    """BASELINE configs[4]: V training on (partial schedule, simulated cost)
+    pairs over VGG-16, data parallel.  Per rank (untimed): complete random
+    schedules on the device (search.random_schedule walk), their simulated
+    costs from the device cost oracle (cost_oracle.benchmark), and every
+    prefix of each schedule as a pair (learner.bootstrap without the
+    cross-schedule min-aggregation), rows featurized once per schedule.
+    Timed: K SGD steps of a per-rank minibatch - gradients on the device,
+    NCCL all-reduce of the 6,305-double gradient, clip + update."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2011_14486_b200 import _lib
+    from paper_2011_14486_b200.cost_oracle import MachineModel, cost_descriptor
+    from paper_2011_14486_b200.trainer import DeviceGradients, flat_params
+    T = inf.T
+    S = max(1, args.train_pairs // (T + 1))
+    seed0 = 10_000_000 + rank * S
+    recs = torch.empty(S * T * 16, dtype=torch.uint8, device=dev)
+    ctx.check(ctx.lib.ts_generate_schedules_device(ctx.h, pid, seed0, S, recs.data_ptr()))
+    offs = torch.arange(0, (S + 1) * T, T, dtype=torch.int64, device=dev)
+    # simulated costs (device cost oracle; host-buffer API, untimed)
+    h_recs = recs.cpu().numpy()
+    h_offs = offs.cpu().numpy()
+    cd = cost_descriptor(inf.p)
+    limbs = np.empty((S, 4), dtype=np.uint64)
+    mw = MachineModel().words()
+    ctx.check(ctx.lib.ts_benchmark(ctx.h, pid, _lib._p(cd), cd.size, _lib._p(mw), _lib._p(h_recs),
+                                   _lib._p(h_offs), S, _lib._p(limbs)))
+    millis = [sum(int(limbs[i, k]) << (64 * k) for k in range(4)) for i in range(S)]
+    logt_s = np.log(np.array([m / 1000.0 for m in millis]))
+    rows = torch.empty((S * T, 16), dtype=torch.float64, device=dev)
+    ctx.check(ctx.lib.ts_featurize_rows_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), S,
+                                               rows.data_ptr()))
+    init = torch.empty((T, 16), dtype=torch.float64, device=dev)
+    ctx.check(ctx.lib.ts_init_rows(ctx.h, pid, 1, init.data_ptr()))
+    N = S * (T + 1)
+    sched = torch.arange(S, dtype=torch.int64, device=dev).repeat_interleave(T + 1)
+    depth = torch.arange(T + 1, dtype=torch.int32, device=dev).repeat(S)
+    row_base = sched * T
+    init_base = torch.zeros(N, dtype=torch.int32, device=dev)
+    Tl = torch.full((N,), T, dtype=torch.int32, device=dev)
+    logt = torch.from_numpy(logt_s).to(dev)[sched]
+    g = DeviceGradients.from_device(ctx, rows.data_ptr(), S * T, init.data_ptr(), T, row_base.data_ptr(),
+                                    init_base.data_ptr(), Tl.data_ptr(), depth.data_ptr(),
+                                    logt.data_ptr(), N, params.hidden)
+    g.set_params(flat_params(params))
+    B = args.train_batch
+    rng = np.random.Generator(np.random.PCG64(1234 + rank))
+    gbuf = torch.zeros(g.n_params, dtype=torch.float64, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.lib.ts_stream(ctx.h), device=dev)
+
+    def step():
+        idx = rng.integers(0, N, size=B).astype(np.int32)
+        g.grads(idx, B * world, params.target_scale, gbuf.data_ptr())
+        if world > 1:
+            g.sync()
+            dist.all_reduce(gbuf)
+            torch.cuda.synchronize(dev)
+        g.apply(1e-3, 5.0, gbuf.data_ptr())
+
+    for _ in range(3):
+        step()
+    g.sync()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = max(5, args.steps * 2)
+    e0.record(stream)
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    g.sync()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    final = g.get_params()
+    assert np.all(np.isfinite(final))
+    return {"metric": "V-training samples/sec", "value": B * world * K / (ms / 1e3),
+            "unit": "samples/s", "pairs_per_gpu": N, "schedules_per_gpu": S, "batch_per_gpu": B,
+            "global_batch": B * world, "steps": K, "ms_per_step": ms / K, "dtype": "f64",
+            "parallelism": f"dp{world}", "collective": "NCCL all_reduce(sum) of the gradient"
+                                                       if world > 1 else "none",
+            "targets": "device cost oracle (cost_oracle.benchmark) of each prefix's schedule"}
 
 
 # --------------------------------------------------------------- GPU arm
@@ -329,6 +420,10 @@ def main():
     roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU-bound (XU pipe 89% "
                     "in ncu), k_featurize_rows is issue/divergence-bound (profiles/r01_ncu.md)")
 
+    train_line = None
+    if not args.no_train:
+        train_line = train_throughput(ctx, pid, inf, params, rank, world, dev, args)
+
     greedy = {}
     if rank == 0 and not args.no_greedy:
         from paper_2011_14486_b200.search import greedy_schedule_gpu
@@ -371,6 +466,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "greedy_wall_s": greedy,
+            "v_training": train_line,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -147,6 +147,13 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
 int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n_states,
                               ts_decision* d_records, int64_t* d_offsets, int64_t* n_records);
 
+/* Normalized f64 rows of the scheduled stages of device-resident states
+ * (rows[offsets[i] + j] = decision j of state i), and the [T][16] rows of
+ * the all-unscheduled state (normalized or raw, host or device pointer). */
+int ts_featurize_rows_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,
+                             const int64_t* d_offsets, int64_t n_states, double* d_rows);
+int ts_init_rows(ts_ctx* ctx, int pipeline_id, int normalized, double* out);
+
 /* Complete random schedules (search.random_schedule, search.py:136-142):
  * schedule i uses SearchRng(seed0 + i); records at d_records[i*T .. i*T+T). */
 int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
@@ -164,11 +171,15 @@ int ts_benchmark(ts_ctx* ctx, int pipeline_id, const int64_t* cost_desc, int64_t
 
 /* ---- V training (value_model.train / gradients, value_model.py:182-293;
  * lstm_forward_cached / lstm_backward, _recurrent_np.py:38-96).
- * The dataset is uploaded once as normalized matrices X[N][Tmax][16] with
- * per-entry lengths and log targets; parameters are a flat f64 vector
- * [Wx 16x4H | Wh Hx4H | b 4H | w H | b_out] resident on the device. */
-int ts_train_load(ts_ctx* ctx, const double* X, const int32_t* Tlen, const double* logt, int64_t N,
-                  int Tmax, int hidden);
+ * Dataset: sample i's input at timestep t is init[init_base[i] + t] when
+ * t < Tlen[i] - depth[i] (unscheduled stages) and rows[row_base[i] + Tlen[i]-1-t]
+ * otherwise (scheduled rows in decision order; all prefixes of a schedule
+ * share its rows).  Rows are normalized f64.  device_ptrs = 1: the arrays are
+ * device pointers (copied device-to-device).  Parameters are a flat f64
+ * vector [Wx 16x4H | Wh Hx4H | b 4H | w H | b_out] resident on the device. */
+int ts_train_load(ts_ctx* ctx, const double* rows, int64_t n_rows, const double* init, int64_t n_init,
+                  const int64_t* row_base, const int32_t* init_base, const int32_t* Tlen,
+                  const int32_t* depth, const double* logt, int64_t N, int hidden, int device_ptrs);
 int ts_train_set_params(ts_ctx* ctx, const double* flat, int64_t n);
 int ts_train_get_params(ts_ctx* ctx, double* flat, int64_t n);
 /* gradient of the loss over idx[0..B) of a minibatch of global size n_total

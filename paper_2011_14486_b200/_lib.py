@@ -80,7 +80,9 @@ def load_library():
             "ts_kernel_times": ([vp, vp, vp, i32], i32),
             "ts_generate_schedules_device": ([vp, i32, ctypes.c_uint64, i64, vp], i32),
             "ts_benchmark": ([vp, i32, vp, i64, vp, vp, vp, i64, vp], i32),
-            "ts_train_load": ([vp, vp, vp, vp, i64, i32, i32], i32),
+            "ts_featurize_rows_device": ([vp, i32, vp, vp, i64, vp], i32),
+            "ts_init_rows": ([vp, i32, i32, vp], i32),
+            "ts_train_load": ([vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, i64, i32, i32], i32),
             "ts_train_set_params": ([vp, vp, i64], i32),
             "ts_train_get_params": ([vp, vp, i64], i32),
             "ts_train_grads": ([vp, vp, i64, i64, f64, vp, vp], i32),

@@ -118,7 +118,8 @@ struct ts_ctx {
   // V training (ts_train_*)
   int tr_H = 0, tr_Tmax = 0;
   int64_t tr_N = 0;
-  DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm;
+  DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm, tr_partial;
+  tr::Data tr_data{};
 };
 
 namespace {
@@ -924,6 +925,38 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   return TS_OK;
 }
 
+int ts_featurize_rows_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,
+                             const int64_t* d_offsets, int64_t n_states, double* d_rows) {
+  if (!ctx || !d_records || !d_offsets || !d_rows || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
+      P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(), ctx->mean.as<double>(),
+      ctx->stdv.as<double>(), d_rows, ctx->status.as<int>());
+  TS_LAUNCHED();
+  return check_device_status(ctx);
+}
+
+int ts_init_rows(ts_ctx* ctx, int pipeline_id, int normalized, double* out) {
+  if (!ctx || !out) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  const int T = P->h->n_stages;
+  TS_CUDA(cudaMemcpyAsync(out, normalized ? P->init_norm.p : P->init_raw.p, sizeof(double) * T * F,
+                          cudaMemcpyDefault, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TS_OK;
+}
+
 int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
                                  ts_decision* d_records) {
   if (!ctx || !d_records || n < 0) return TS_ERR_ARG;
@@ -1024,22 +1057,44 @@ int ts_generate_states_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int6
 }
 
 // ------------------------------------------------------------------ training
-int ts_train_load(ts_ctx* ctx, const double* X, const int32_t* Tlen, const double* logt, int64_t N, int Tmax,
-                  int hidden) {
-  if (!ctx || !X || !Tlen || !logt || N < 1 || Tmax < 1) return TS_ERR_ARG;
+int ts_train_load(ts_ctx* ctx, const double* rows, int64_t n_rows, const double* init, int64_t n_init,
+                  const int64_t* row_base, const int32_t* init_base, const int32_t* Tlen,
+                  const int32_t* depth, const double* logt, int64_t N, int hidden, int device_ptrs) {
+  if (!ctx || !rows || !row_base || !init_base || !Tlen || !depth || !logt || N < 1 || n_rows < 1)
+    return TS_ERR_ARG;
   TS_NEED_DEVICE();
   if (hidden < 1 || hidden > 32) return fail(ctx, TS_ERR_ARG, "hidden size must be in 1..32");
   TS_CUDA(cudaSetDevice(ctx->device));
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  std::vector<int32_t> hT(N);
+  TS_CUDA(cudaMemcpy(hT.data(), Tlen, sizeof(int32_t) * N, device_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  int Tmax = 1;
+  for (int64_t i = 0; i < N; ++i) Tmax = std::max(Tmax, (int)hT[i]);
   ctx->tr_H = hidden;
   ctx->tr_Tmax = Tmax;
   ctx->tr_N = N;
-  TS_CUDA(ctx->tr_X.reserve(sizeof(double) * N * Tmax * F));
-  TS_CUDA(ctx->tr_T.reserve(sizeof(int32_t) * N));
+  TS_CUDA(ctx->tr_X.reserve(sizeof(double) * (n_rows + std::max<int64_t>(n_init, 1)) * F));
+  TS_CUDA(ctx->tr_T.reserve((sizeof(int64_t) + 3 * sizeof(int32_t)) * N));
   TS_CUDA(ctx->tr_logt.reserve(sizeof(double) * N));
-  TS_CUDA(cudaMemcpy(ctx->tr_X.p, X, sizeof(double) * N * Tmax * F, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->tr_T.p, Tlen, sizeof(int32_t) * N, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->tr_logt.p, logt, sizeof(double) * N, cudaMemcpyHostToDevice));
+  double* drows = ctx->tr_X.as<double>();
+  double* dinit = drows + n_rows * F;
+  int64_t* drb = ctx->tr_T.as<int64_t>();
+  int32_t* dib = reinterpret_cast<int32_t*>(drb + N);
+  TS_CUDA(cudaMemcpy(drows, rows, sizeof(double) * n_rows * F, kind));
+  if (n_init) TS_CUDA(cudaMemcpy(dinit, init, sizeof(double) * n_init * F, kind));
+  TS_CUDA(cudaMemcpy(drb, row_base, sizeof(int64_t) * N, kind));
+  TS_CUDA(cudaMemcpy(dib, init_base, sizeof(int32_t) * N, kind));
+  TS_CUDA(cudaMemcpy(dib + N, Tlen, sizeof(int32_t) * N, kind));
+  TS_CUDA(cudaMemcpy(dib + 2 * N, depth, sizeof(int32_t) * N, kind));
+  TS_CUDA(cudaMemcpy(ctx->tr_logt.p, logt, sizeof(double) * N, kind));
+  ctx->tr_data.rows = drows;
+  ctx->tr_data.init = dinit;
+  ctx->tr_data.row_base = drb;
+  ctx->tr_data.init_base = dib;
+  ctx->tr_data.Tlen = dib + N;
+  ctx->tr_data.depth = dib + 2 * N;
+  ctx->tr_data.logt = ctx->tr_logt.as<double>();
   const tr::Layout L(hidden);
   TS_CUDA(ctx->tr_P.reserve(sizeof(double) * L.n));
   TS_CUDA(ctx->tr_grad.reserve(sizeof(double) * L.n));
@@ -1072,9 +1127,7 @@ static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs&
   TS_CUDA(ctx->tr_raw.reserve(sizeof(double) * B));
   TS_CUDA(ctx->tr_draw.reserve(sizeof(double) * B));
   TS_CUDA(cudaMemcpyAsync(ctx->tr_batch.p, idx, sizeof(int32_t) * B, cudaMemcpyHostToDevice, ctx->stream));
-  a.X = ctx->tr_X.as<double>();
-  a.Tlen = ctx->tr_T.as<int>();
-  a.logt = ctx->tr_logt.as<double>();
+  a.D = ctx->tr_data;
   a.batch = ctx->tr_batch.as<int>();
   a.P = ctx->tr_P.as<double>();
   a.cache = nullptr;
@@ -1115,7 +1168,13 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
   a.n_total = (double)n_total;
   tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
   TS_LAUNCHED();
-  tr::k_train_wgrad<<<(L.n + 255) / 256, 256, 0, ctx->stream>>>(a, grad);
+  const int64_t K = (int64_t)ctx->tr_Tmax * B;
+  const int ksplit = (int)std::min<int64_t>(64, std::max<int64_t>(1, K / 512));
+  TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
+  tr::k_train_wgrad<<<dim3((L.n + 255) / 256, ksplit), 256, 0, ctx->stream>>>(a, ksplit,
+                                                                             ctx->tr_partial.as<double>());
+  TS_LAUNCHED();
+  tr::k_train_reduce<<<(L.n + 255) / 256, 256, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
   TS_LAUNCHED();
   if (raw_out) {
     TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));

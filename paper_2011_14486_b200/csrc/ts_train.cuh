@@ -6,16 +6,22 @@
 // throughout so the device trajectory tracks the reference's (the training
 // loop is contractive: 1e-12 perturbations stay ~1e-13).
 //
+// Dataset layout: a sample is (rows, init, T, d): its input at timestep t is
+// init[init_base + t] for t < T - d (unscheduled stages) and
+// rows[row_base + (T - 1 - t)] otherwise (the scheduled stages' rows in
+// decision order).  All prefixes of one complete schedule share its rows,
+// so a bootstrap-style dataset of T+1 prefixes per schedule stores T rows.
+//
 //   k_train_fb     warp per sequence, lane per hidden unit: forward with the
 //                  activation cache, d_raw = 2(raw + ts - log t)/n_total,
 //                  BPTT; writes dz[b][t][4H] and keeps h_prev/h in the cache
-//   k_train_wgrad  thread per parameter: dWx = sum x^T dz, dWh = sum h_prev^T dz,
-//                  db = sum dz, dw = sum h d_raw, db_out = sum_b T_b d_raw_b,
-//                  reduced over (t descending, b) in a fixed order
+//   k_train_wgrad  split-K weight gradients: block (p-tile, k-split) sums its
+//                  (t, b) range in a fixed order into partials
+//   k_train_reduce partials summed in split order -> grad
 //   k_train_apply  one block: global L2 norm incl. b_out, clip, p -= lr g
 //   k_train_fwd    warp per sequence: raw for _eval_split
 //
-// The gradient buffer is a plain device array between k_train_wgrad and
+// The gradient buffer is a plain device array between k_train_reduce and
 // k_train_apply, so data-parallel training all-reduces it (NCCL) in between.
 #pragma once
 
@@ -41,10 +47,22 @@ constexpr int CACHE_FIELDS = 8;
 
 __device__ __forceinline__ double sig(double x) { return fdiv(1.0, fadd(1.0, exp(-x))); }
 
+struct Data {
+  const double* rows;       // [n_rows][16] normalized
+  const double* init;       // [n_init][16] normalized
+  const int64_t* row_base;  // [N]
+  const int32_t* init_base; // [N]
+  const int32_t* Tlen;      // [N]
+  const int32_t* depth;     // [N]
+  const double* logt;       // [N]
+  __device__ __forceinline__ const double* x(int64_t i, int t) const {
+    const int T = Tlen[i], d = depth[i];
+    return t < T - d ? init + (int64_t)(init_base[i] + t) * F : rows + (row_base[i] + (T - 1 - t)) * F;
+  }
+};
+
 struct TrainArgs {
-  const double* X;      // [N][Tmax][16] normalized
-  const int* Tlen;      // [N]
-  const double* logt;   // [N]
+  Data D;
   const int* batch;     // [B] dataset indices
   const double* P;      // params
   double* cache;        // [B][Tmax][8][H]
@@ -65,8 +83,7 @@ __global__ void k_train_fb(TrainArgs a) {
   const bool act = lane < H;
   const int j = act ? lane : 0;
   const int idx = a.batch[wb];
-  const int T = a.Tlen[idx];
-  const double* X = a.X + (int64_t)idx * a.Tmax * F;
+  const int T = a.D.Tlen[idx];
   const double* Wx = a.P + L.oWx;
   const double* Wh = a.P + L.oWh;
   const double* bb = a.P + L.ob;
@@ -76,9 +93,10 @@ __global__ void k_train_fb(TrainArgs a) {
   double raw = fmul((double)T, a.P[L.obout]);
   // ---- forward with cache (_recurrent_np.py:38-59)
   for (int t = 0; t < T; ++t) {
+    const double* X = a.D.x(idx, t);
     double zi = bb[j], zf = bb[H + j], zg = bb[2 * H + j], zo = bb[3 * H + j];
     for (int k = 0; k < F; ++k) {
-      const double xv = X[t * F + k];
+      const double xv = X[k];
       const double* wr = Wx + k * G;
       zi = fadd(zi, fmul(xv, wr[j]));
       zf = fadd(zf, fmul(xv, wr[H + j]));
@@ -116,7 +134,7 @@ __global__ void k_train_fb(TrainArgs a) {
     raw = fadd(raw, acc);
   }
   // d_raw = 2 (raw + ts - log t) / n  (value_model.py:201)
-  const double d_raw = fdiv(fmul(2.0, fsub(fadd(raw, a.target_scale), a.logt[idx])), a.n_total);
+  const double d_raw = fdiv(fmul(2.0, fsub(fadd(raw, a.target_scale), a.D.logt[idx])), a.n_total);
   if (lane == 0) {
     a.raw[wb] = raw;
     a.draw[wb] = d_raw;
@@ -158,48 +176,52 @@ __global__ void k_train_fb(TrainArgs a) {
   }
 }
 
-// Weight gradients: thread per parameter, fixed reduction order (t
-// descending, then batch order) - deterministic for a given batch.
-__global__ void k_train_wgrad(TrainArgs a, double* __restrict__ grad) {
+// Split-K weight gradients.  The reduction axis is the (t descending, b)
+// sequence of valid (sequence, timestep) pairs; block y handles a fixed
+// contiguous range of it (identical split for a given batch -> deterministic).
+__global__ void k_train_wgrad(TrainArgs a, int ksplit, double* __restrict__ partial) {
   const Layout L(a.H);
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= L.n) return;
   const int H = a.H, G = L.G;
+  const int64_t K = (int64_t)a.Tmax * a.B;
+  const int64_t k0 = K * blockIdx.y / ksplit, k1 = K * (blockIdx.y + 1) / ksplit;
   double acc = 0.0;
-  if (p < L.oWh) {  // dWx[k][c] = sum x[t][k] dz[t][c]
-    const int k = p / G, c = p % G;
-    for (int t = a.Tmax - 1; t >= 0; --t)
-      for (int b = 0; b < a.B; ++b) {
-        const int idx = a.batch[b];
-        if (t >= a.Tlen[idx]) continue;
-        acc = fadd(acc, fmul(a.X[((int64_t)idx * a.Tmax + t) * F + k], a.dz[((int64_t)b * a.Tmax + t) * G + c]));
-      }
-  } else if (p < L.ob) {  // dWh[k][c] = sum h_prev[t][k] dz[t][c]
-    const int q = p - L.oWh, k = q / G, c = q % G;
-    for (int t = a.Tmax - 1; t >= 0; --t)
-      for (int b = 0; b < a.B; ++b) {
-        if (t >= a.Tlen[a.batch[b]]) continue;
-        const double hp = a.cache[(((int64_t)b * a.Tmax + t) * CACHE_FIELDS + 5) * H + k];
-        acc = fadd(acc, fmul(hp, a.dz[((int64_t)b * a.Tmax + t) * G + c]));
-      }
-  } else if (p < L.ow) {  // db[c] = sum dz[t][c]
-    const int c = p - L.ob;
-    for (int t = a.Tmax - 1; t >= 0; --t)
-      for (int b = 0; b < a.B; ++b) {
-        if (t >= a.Tlen[a.batch[b]]) continue;
-        acc = fadd(acc, a.dz[((int64_t)b * a.Tmax + t) * G + c]);
-      }
-  } else if (p < L.obout) {  // dw[j] = sum h[t][j] d_raw
-    const int jj = p - L.ow;
-    for (int t = a.Tmax - 1; t >= 0; --t)
-      for (int b = 0; b < a.B; ++b) {
-        if (t >= a.Tlen[a.batch[b]]) continue;
-        const double hv = a.cache[(((int64_t)b * a.Tmax + t) * CACHE_FIELDS + 7) * H + jj];
-        acc = fadd(acc, fmul(hv, a.draw[b]));
-      }
-  } else {  // db_out = sum_b T_b d_raw_b
-    for (int b = 0; b < a.B; ++b) acc = fadd(acc, fmul((double)a.Tlen[a.batch[b]], a.draw[b]));
+  int kind, r, col;
+  if (p < L.oWh) { kind = 0; r = p / G; col = p % G; }
+  else if (p < L.ob) { kind = 1; r = (p - L.oWh) / G; col = (p - L.oWh) % G; }
+  else if (p < L.ow) { kind = 2; r = 0; col = p - L.ob; }
+  else if (p < L.obout) { kind = 3; r = p - L.ow; col = 0; }
+  else { kind = 4; r = 0; col = 0; }
+  for (int64_t kk = k0; kk < k1; ++kk) {
+    const int t = a.Tmax - 1 - (int)(kk / a.B);
+    const int b = (int)(kk % a.B);
+    const int idx = a.batch[b];
+    const int T = a.D.Tlen[idx];
+    if (kind == 4) {  // db_out = sum_b T_b d_raw_b, counted once per sequence (at t = 0)
+      if (t == 0) acc = fadd(acc, fmul((double)T, a.draw[b]));
+      continue;
+    }
+    if (t >= T) continue;
+    const int64_t bt = (int64_t)b * a.Tmax + t;
+    if (kind == 0) {
+      acc = fadd(acc, fmul(a.D.x(idx, t)[r], a.dz[bt * G + col]));
+    } else if (kind == 1) {
+      acc = fadd(acc, fmul(a.cache[(bt * CACHE_FIELDS + 5) * H + r], a.dz[bt * G + col]));
+    } else if (kind == 2) {
+      acc = fadd(acc, a.dz[bt * G + col]);
+    } else {
+      acc = fadd(acc, fmul(a.cache[(bt * CACHE_FIELDS + 7) * H + r], a.draw[b]));
+    }
   }
+  partial[(int64_t)blockIdx.y * L.n + p] = acc;
+}
+
+__global__ void k_train_reduce(const double* __restrict__ partial, int ksplit, int n, double* __restrict__ grad) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double acc = 0.0;
+  for (int k = 0; k < ksplit; ++k) acc = fadd(acc, partial[(int64_t)k * n + p]);
   grad[p] = acc;
 }
 
@@ -227,7 +249,8 @@ __global__ void k_train_apply(double* __restrict__ P, const double* __restrict__
   if (threadIdx.x == 0 && norm_out) *norm_out = norm;
 }
 
-// raw for a list of sequences (eval): warp per sequence
+// raw for a list of sequences (eval, Cython order with the zero skip):
+// warp per sequence
 __global__ void k_train_fwd(TrainArgs a) {
   const int wb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -237,8 +260,7 @@ __global__ void k_train_fwd(TrainArgs a) {
   const bool act = lane < H;
   const int j = act ? lane : 0;
   const int idx = a.batch[wb];
-  const int T = a.Tlen[idx];
-  const double* X = a.X + (int64_t)idx * a.Tmax * F;
+  const int T = a.D.Tlen[idx];
   const double* Wx = a.P + L.oWx;
   const double* Wh = a.P + L.oWh;
   const double* bb = a.P + L.ob;
@@ -246,9 +268,10 @@ __global__ void k_train_fwd(TrainArgs a) {
   double h = 0.0, c = 0.0;
   double raw = fmul((double)T, a.P[L.obout]);
   for (int t = 0; t < T; ++t) {
+    const double* X = a.D.x(idx, t);
     double zi = bb[j], zf = bb[H + j], zg = bb[2 * H + j], zo = bb[3 * H + j];
     for (int k = 0; k < F; ++k) {
-      const double xv = X[t * F + k];
+      const double xv = X[k];
       if (xv != 0.0) {
         const double* wr = Wx + k * G;
         zi = fadd(zi, fmul(xv, wr[j]));

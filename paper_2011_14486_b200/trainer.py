@@ -55,17 +55,38 @@ def shard(batch: np.ndarray, rank: int, world: int) -> np.ndarray:
 
 
 class DeviceGradients:
-    """ts_train_* wrapper: dataset resident on the device."""
+    """ts_train_* wrapper: dataset resident on the device.
+
+    Host form: per-sample normalized matrices (full depth).  Device form
+    (`from_device`): shared scheduled rows + prefix depths (bench)."""
 
     def __init__(self, ctx, X, Tlen, logt, hidden):
         self.ctx = ctx
         self.hidden = hidden
         self.n_params = 16 * 4 * hidden + hidden * 4 * hidden + 4 * hidden + hidden + 1
+        if X is None:
+            return
         X = np.ascontiguousarray(X, dtype=np.float64)
-        self._T = np.ascontiguousarray(Tlen, dtype=np.int32)
-        ctx.check(ctx.lib.ts_train_load(ctx.h, _lib._p(X), _lib._p(self._T),
-                                        _lib._p(np.ascontiguousarray(logt, dtype=np.float64)),
-                                        X.shape[0], X.shape[1], hidden))
+        T = np.ascontiguousarray(Tlen, dtype=np.int32)
+        # sample i: rows[base_i + j] = its row of decision j = X[i, T_i - 1 - j]
+        base = np.zeros(len(T), dtype=np.int64)
+        np.cumsum(T[:-1], out=base[1:])
+        rows = np.concatenate([X[i, : T[i]][::-1] for i in range(len(T))])
+        rows = np.ascontiguousarray(rows)
+        zeros = np.zeros(len(T), dtype=np.int32)
+        ctx.check(ctx.lib.ts_train_load(
+            ctx.h, _lib._p(rows), rows.shape[0], None, 0, _lib._p(base), _lib._p(zeros),
+            _lib._p(T), _lib._p(T.copy()), _lib._p(np.ascontiguousarray(logt, dtype=np.float64)),
+            len(T), hidden, 0))
+
+    @classmethod
+    def from_device(cls, ctx, d_rows, n_rows, d_init, n_init, d_row_base, d_init_base, d_T, d_depth,
+                    d_logt, N, hidden):
+        self = cls(ctx, None, None, None, hidden)
+        c = ctypes.c_void_p
+        ctx.check(ctx.lib.ts_train_load(ctx.h, c(d_rows), n_rows, c(d_init), n_init, c(d_row_base),
+                                        c(d_init_base), c(d_T), c(d_depth), c(d_logt), N, hidden, 1))
+        return self
 
     def set_params(self, flat):
         flat = np.ascontiguousarray(flat, dtype=np.float64)
