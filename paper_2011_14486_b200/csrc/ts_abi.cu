@@ -633,7 +633,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
-          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>());
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>(),
+          perm);
       TS_LAUNCHED();
     }
     tc::TcArgs ta;

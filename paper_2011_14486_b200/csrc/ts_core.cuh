@@ -425,22 +425,49 @@ TS_HD bool anchor_ok(const Nest& c, int lvl) {
 // Returns TS_OK / TS_ERR_OVERFLOW.
 TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& cn, int lvl,
                            int64_t* pe, u256& inv, int& depth) {
-  inv = cn.inv;
+  // invocations = consumer invocations * prod(outer loop extents up to lvl);
+  // a 64-bit fast path covers the common case, 256 bits the deep chains
   bool ok = true;
-  int64_t rem[TS_MAX_PURE + TS_MAX_RED];
+  {
+    uint64_t p = cn.inv.w[0];
+    bool small = u256_small(cn.inv);
 #pragma unroll
-  for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd) rem[dd] = 1;
+    for (int j = 0; j < TS_MAX_LOOPS; ++j) {
+      if (j <= lvl && j < cn.n_loops) {
+#ifdef __CUDA_ARCH__
+        small = small && __umul64hi(p, cn.ext[j]) == 0;
+#else
+        small = small && ((unsigned __int128)p * cn.ext[j]) >> 64 == 0;
+#endif
+        p *= cn.ext[j];
+      }
+    }
+    if (small) {
+      inv = u256_from(p);
+    } else {
+      inv = cn.inv;
+#pragma unroll
+      for (int j = 0; j < TS_MAX_LOOPS; ++j)
+        if (j <= lvl && j < cn.n_loops) ok = u256_mul_u64(inv, cn.ext[j]) && ok;
+    }
+  }
+  // per-invocation consumer region: for each consumer dim read by an edge,
+  // the product of that dim's loops strictly inside lvl.  Extents are below
+  // 2^31 (descriptor-checked) and so are these products (<= full extents).
+  uint32_t rv[2][TS_MAX_PURE];
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int k = 0; k < TS_MAX_PURE; ++k) rv[e][k] = 1u;
 #pragma unroll
   for (int j = 0; j < TS_MAX_LOOPS; ++j) {
-    if (j >= cn.n_loops) continue;
-    if (j <= lvl) {
-      ok = u256_mul_u64(inv, cn.ext[j]) && ok;
-    } else {
-      const int dim = loop_dim(cn.id[j], cs.n_pure);
+    const uint32_t m = (j > lvl && j < cn.n_loops) ? cn.ext[j] : 1u;
+    const int dim = loop_dim(cn.id[j], cs.n_pure);
 #pragma unroll
-      for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd)
-        if (dd == dim) rem[dd] *= cn.ext[j];
-    }
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int k = 0; k < TS_MAX_PURE; ++k)
+        if (s.cdim[e][k] == dim) rv[e][k] *= m;
   }
 #pragma unroll
   for (int k = 0; k < TS_MAX_PURE; ++k) {
@@ -449,11 +476,7 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& 
     for (int e = 0; e < 2; ++e) {
       if (e >= s.n_cedges) continue;
       const int cd = s.cdim[e][k];
-      int64_t rv = 1;
-#pragma unroll
-      for (int dd = 0; dd < TS_MAX_PURE + TS_MAX_RED; ++dd)
-        if (dd == cd) rv = rem[dd];
-      const int64_t ext = cd < 0 ? s.cwindow[e][k] : s.cstride[e][k] * (rv - 1) + s.cwindow[e][k];
+      const int64_t ext = cd < 0 ? s.cwindow[e][k] : s.cstride[e][k] * ((int64_t)rv[e][k] - 1) + s.cwindow[e][k];
       best = ext > best ? ext : best;
     }
     pe[k] = best;
@@ -578,11 +601,27 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
 #pragma unroll
   for (int k = 0; k < TS_MAX_PURE; ++k)
     if (k < s.n_pure) region *= (uint64_t)pe[k];
-  u256 num = n.inv;
-  bool ok = u256_mul_u64(num, region);
-  ok = u256_mul_u64(num, s.red_points) && ok;
-  if (!ok) return TS_ERR_OVERFLOW;
-  f[5] = glibc_log2(u256_div_to_double(num, s.dp));
+  bool fast = u256_small(n.inv);
+  uint64_t p = n.inv.w[0];
+#ifdef __CUDA_ARCH__
+  fast = fast && __umul64hi(p, region) == 0;
+  p *= region;
+  fast = fast && __umul64hi(p, s.red_points) == 0;
+#else
+  fast = fast && ((unsigned __int128)p * region) >> 64 == 0;
+  p *= region;
+  fast = fast && ((unsigned __int128)p * s.red_points) >> 64 == 0;
+#endif
+  p *= s.red_points;
+  if (fast && p <= (1ull << 53) && s.dp.d <= (1ull << 53)) {
+    f[5] = glibc_log2(fdiv(u64_to_double(p), u64_to_double(s.dp.d)));  // both exact
+  } else {
+    u256 num = n.inv;
+    bool ok = u256_mul_u64(num, region);
+    ok = u256_mul_u64(num, s.red_points) && ok;
+    if (!ok) return TS_ERR_OVERFLOW;
+    f[5] = glibc_log2(u256_div_to_double(num, s.dp));
+  }
   // working set at the store site (cost_oracle.py:162-169), cache 32768
   const uint64_t pts = (d.flags & TS_FLAG_STORE_AT) ? region : s.pure_points;
   f[6] = pts <= 8192u ? 1.0 : 0.0;  // 4 * pts <= 32768, overflow-free
