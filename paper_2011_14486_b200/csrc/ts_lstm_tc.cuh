@@ -122,9 +122,7 @@ __device__ __forceinline__ float rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// u = -z log2 e  ->  sigma(z);   v = -2 z log2 e  ->  tanh(z)
-__device__ __forceinline__ float sig_u(float u) { return rcp(1.0f + ex2(u)); }
-__device__ __forceinline__ float tanh_v(float v) { return fmaf(2.0f, rcp(1.0f + ex2(v)), -1.0f); }
+__device__ __forceinline__ float clamp40(float x) { return fminf(fmaxf(x, -40.0f), 40.0f); }
 
 // hi/lo fp16 split of 8 floats into two 16-byte chunks
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
@@ -320,13 +318,21 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
         float h8[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
+          // With t_x = 1 + 2^u_x:  sigma = 1/t,  tanh = (1 - 2^v)/(1 + 2^v), so
+          //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
+          //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c))
+          // 5 ex2 + 2 rcp per unit instead of 5 + 5.  Exponents are clamped
+          // to +-40 (sigma saturates to 1 - 2^-40 / 2^-40) so the products
+          // stay finite in fp32.
           const int j = g8 * 8 + u;
-          const float gi = sig_u(ui[u]);
-          const float gf = sig_u(uf[u]);
-          const float gg = tanh_v(vg[u]);
-          const float go = sig_u(uo[u]);
-          c[j] = fmaf(gf, c[j], gi * gg);
-          h8[u] = go * tanh_v(c2 * c[j]);
+          const float ei = ex2(clamp40(ui[u])), ef = ex2(clamp40(uf[u]));
+          const float eg = ex2(clamp40(vg[u])), eo = ex2(clamp40(uo[u]));
+          const float ti = 1.0f + ei, tf = 1.0f + ef, tg = 1.0f + eg;
+          const float tig = ti * tg;
+          const float num = fmaf(c[j], tig, (1.0f - eg) * tf);
+          c[j] = num * rcp(tf * tig);
+          const float ec = ex2(clamp40(c2 * c[j]));
+          h8[u] = (1.0f - ec) * rcp((1.0f + eo) * (1.0f + ec));
           acc = fmaf(h8[u], wout[j], acc);
         }
         // the UMMA that read A has completed (mbarrier), so h can go straight in
