@@ -124,6 +124,28 @@ __device__ __forceinline__ float rcp(float x) {
 }
 __device__ __forceinline__ float clamp40(float x) { return fminf(fmaxf(x, -40.0f), 40.0f); }
 
+// 2^x on the FMA/ALU pipes (relieves the MUFU pipe, the LSTM's binding
+// unit): round-to-nearest split x = j + f with the 1.5*2^23 trick,
+// degree-5 near-minimax polynomial for 2^f on [-1/2, 1/2] (max rel err
+// 2.3e-7, the same order as ex2.approx), exponent add.  |x| <= 40.
+__device__ __forceinline__ float ex2_fma(float x) {
+  const float t = __fadd_rn(x, 12582912.0f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  float p = fmaf(0.0013276466634124517f, f, 0.009675540961325169f);
+  p = fmaf(p, f, 0.05550713464617729f);
+  p = fmaf(p, f, 0.24022120237350464f);
+  p = fmaf(p, f, 0.6931469440460205f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+#ifndef TS_FMA_EXP
+#define TS_FMA_EXP 0  // how many of the 5 per-unit exponentials use ex2_fma
+#endif
+__device__ __forceinline__ float ex2_sel(float x, int slot) {
+  return slot < TS_FMA_EXP ? ex2_fma(x) : ex2(x);
+}
+
 // hi/lo fp16 split of 8 floats into two 16-byte chunks
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
@@ -325,13 +347,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           // to +-40 (sigma saturates to 1 - 2^-40 / 2^-40) so the products
           // stay finite in fp32.
           const int j = g8 * 8 + u;
-          const float ei = ex2(clamp40(ui[u])), ef = ex2(clamp40(uf[u]));
-          const float eg = ex2(clamp40(vg[u])), eo = ex2(clamp40(uo[u]));
+          const float ei = ex2_sel(clamp40(ui[u]), 0), ef = ex2_sel(clamp40(uf[u]), 1);
+          const float eg = ex2_sel(clamp40(vg[u]), 2), eo = ex2_sel(clamp40(uo[u]), 3);
           const float ti = 1.0f + ei, tf = 1.0f + ef, tg = 1.0f + eg;
           const float tig = ti * tg;
           const float num = fmaf(c[j], tig, (1.0f - eg) * tf);
           c[j] = num * rcp(tf * tig);
-          const float ec = ex2(clamp40(c2 * c[j]));
+          const float ec = ex2_sel(clamp40(c2 * c[j]), 4);
           h8[u] = (1.0f - ec) * rcp((1.0f + eo) * (1.0f + ec));
           acc = fmaf(h8[u], wout[j], acc);
         }
