@@ -122,7 +122,10 @@ __device__ __forceinline__ float rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float clamp40(float x) { return fminf(fmaxf(x, -40.0f), 40.0f); }
+// Upper clamp only: 2^x for very negative x underflows to 0, which the
+// fused cell algebra tolerates (t = 1); the upper bound keeps the triple
+// products of (1 + 2^x) below 2^128.
+__device__ __forceinline__ float clamp40(float x) { return fminf(x, 40.0f); }
 
 // 2^x on the FMA/ALU pipes (relieves the MUFU pipe, the LSTM's binding
 // unit): round-to-nearest split x = j + f with the 1.5*2^23 trick,
@@ -344,8 +347,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
           //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c))
           // 5 ex2 + 2 rcp per unit instead of 5 + 5.  Exponents are clamped
-          // to +-40 (sigma saturates to 1 - 2^-40 / 2^-40) so the products
-          // stay finite in fp32.
+          // above at 40 (sigma(z) >= 2^-40 instead of smaller) so the
+          // products stay finite in fp32.
           const int j = g8 * 8 + u;
           const float ei = ex2_sel(clamp40(ui[u]), 0), ef = ex2_sel(clamp40(uf[u]), 1);
           const float eg = ex2_sel(clamp40(vg[u]), 2), eo = ex2_sel(clamp40(uo[u]), 3);
