@@ -516,7 +516,8 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const Nest* cn, co
       const int64_t f = k == 0 ? d.split[0] : k == 1 ? d.split[1] : k == 2 ? d.split[2] : d.split[3];
       const int64_t p = sel4(pe, k);
       bad = bad || k >= s.n_pure || (!f && (id & 1));
-      e = f ? ((id & 1) ? f : p / f) : p;
+      // extents < 2^31 (descriptor-checked): 32-bit division
+      e = f ? ((id & 1) ? f : (int64_t)((uint32_t)p / (uint32_t)f)) : p;
     } else {
       const int r = id - 8;
       bad = bad || r >= s.n_red;
