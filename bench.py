@@ -387,10 +387,17 @@ def main():
     h_offs = torch.empty(M + 1, dtype=torch.int64, pin_memory=True)
     h_offs.copy_(offs)
     h_out = torch.empty(M, dtype=torch.float64, pin_memory=True)
+    # the 8-byte wire format (ts_score_states_packed): what predict_states
+    # sends for large batches
+    packed = _lib.pack_records(np.frombuffer(h_recs.numpy().tobytes(), dtype=_lib.DECISION_DTYPE))
+    assert packed is not None
+    h_packed = torch.from_numpy(packed.view(np.int64)).pin_memory()
+    h_depth = torch.from_numpy(np.diff(h_offs.numpy()).astype(np.uint8)).pin_memory()
+    e2e_h2d = int(packed.nbytes + M)
 
     def e2e_step():
-        ctx.check(ctx.lib.ts_score_states(ctx.h, pid, h_recs.data_ptr(), h_offs.data_ptr(), M,
-                                          mode, h_out.data_ptr()))
+        ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, h_packed.data_ptr(), h_depth.data_ptr(), M,
+                                                 mode, h_out.data_ptr()))
 
     for _ in range(2):
         e2e_step()
@@ -483,7 +490,8 @@ def main():
                        "mode": args.mode, "l2": "inputs larger than L2 (records "
                        f"{n_records * 16 / 1e6:.0f} MB/GPU)", "parallelism": f"shard{world}"},
             "e2e": {"value": e2e_value, "unit": "states/s",
-                    "h2d_bytes_per_step": int(n_records * 16 + 8 * (M + 1)),
+                    "h2d_bytes_per_step": e2e_h2d, "wire_format": "8-byte packed decisions + u8 depths "
+                                                                  "(ts_score_states_packed)",
                     "d2h_bytes_per_step": int(8 * M)},
             "gpu_launches": int(launches),
             "roofline": roof,

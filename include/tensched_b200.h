@@ -112,6 +112,16 @@ int ts_featurize_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records
 int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records,
                     const int64_t* offsets, int64_t n_states, int mode, double* out_v);
 
+/* Packed wire format for host callers: one 64-bit word per decision
+ *   bits 0-31 loop ids (4 bits each, position j at 4j), 32-35 n_loops,
+ *   36-51 split code per pure dim (4 bits: index into
+ *   {none,2,3,4,5,6,7,8,12,16,24,32,48,64,128,255}), 52-53 vec code
+ *   (1,4,8,16), 54-55 flags, 56-59 compute_at level + 1 (0 = root)
+ * and one u8 depth per state (offsets are rebuilt on the device): half the
+ * PCIe bytes of ts_score_states. */
+int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed, const uint8_t* depths,
+                           int64_t n_states, int mode, double* out_v);
+
 /* Same with device-resident inputs/outputs (pointers into the context's
  * device), stream-ordered on the context stream. */
 int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,

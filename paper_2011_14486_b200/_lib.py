@@ -33,6 +33,34 @@ DECISION_DTYPE = np.dtype(
 assert DECISION_DTYPE.itemsize == 16
 
 
+SPLIT_TABLE = np.array([0, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 48, 64, 128, 255], dtype=np.uint8)
+_SPLIT_CODE = np.full(256, 255, dtype=np.uint8)
+_SPLIT_CODE[SPLIT_TABLE] = np.arange(16, dtype=np.uint8)
+_VEC_CODE = np.full(256, 255, dtype=np.uint8)
+_VEC_CODE[[1, 4, 8, 16]] = [0, 1, 2, 3]
+
+
+def pack_records(recs: np.ndarray) -> np.ndarray | None:
+    """16-byte ts_decision records -> the 8-byte wire format of
+    ts_score_states_packed (None if a split factor or vector width falls
+    outside the packed tables)."""
+    sc = _SPLIT_CODE[recs["split"]]
+    vc = _VEC_CODE[recs["vec"]]
+    if np.any(sc == 255) or np.any(vc == 255):
+        return None
+    order = recs["order"].astype(np.uint64) & np.uint64(0xF)
+    w = np.zeros(len(recs), dtype=np.uint64)
+    for j in range(8):
+        w |= order[:, j] << np.uint64(4 * j)
+    w |= recs["n_loops"].astype(np.uint64) << np.uint64(32)
+    for k in range(4):
+        w |= sc[:, k].astype(np.uint64) << np.uint64(36 + 4 * k)
+    w |= vc.astype(np.uint64) << np.uint64(52)
+    w |= (recs["flags"].astype(np.uint64) & np.uint64(3)) << np.uint64(54)
+    w |= (recs["anchor"].astype(np.int64) + 1).astype(np.uint64) << np.uint64(56)
+    return w
+
+
 class CudaUnavailableError(PipelineError):
     """The sm_100a extension or a B200 is not available (no CPU fallback)."""
 
@@ -66,6 +94,7 @@ def load_library():
             "ts_featurize_states": ([vp, i32, vp, vp, i64, i32, vp], i32),
             "ts_score_states": ([vp, i32, vp, vp, i64, i32, vp], i32),
             "ts_score_states_device": ([vp, i32, vp, vp, i64, i64, i32, vp], i32),
+            "ts_score_states_packed": ([vp, i32, vp, vp, i64, i32, vp], i32),
             "ts_lstm_forward": ([vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, f64, i32, vp], i32),
             "ts_candidates": ([vp, i32, vp, i64, vp, i64, ctypes.POINTER(i64)], i32),
             "ts_check_action": ([vp, i32, vp, i64, vp], i32),

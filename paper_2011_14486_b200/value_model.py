@@ -28,6 +28,7 @@ from .featurizer import FEATURE_WIDTH, Normalizer
 from .schedule_space import encode_states
 
 INPUT_DIM = FEATURE_WIDTH
+PACKED_MIN = 4096  # batches at least this large travel in the 8-byte wire format
 MODE_EXACT = _lib.MODE_EXACT
 MODE_FAST = _lib.MODE_FAST
 
@@ -79,10 +80,16 @@ def predict_states(params, states, jobs: int = 1, mode: int = MODE_EXACT, device
     for inf, idxs, recs, offsets in encode_states(states):
         pid = ctx.pipeline_id(inf.desc)
         vals = np.empty(len(idxs))
+        packed = _lib.pack_records(recs) if len(idxs) >= PACKED_MIN and inf.T < 256 else None
         with ctx.lock:
-            ctx.check(ctx.lib.ts_score_states(ctx.h, pid, _lib._p(recs) if len(recs) else None,
-                                              _lib._p(offsets), len(idxs), int(mode),
-                                              _lib._p(vals)))
+            if packed is not None:  # half the PCIe bytes (ts_score_states_packed)
+                depths = np.diff(offsets).astype(np.uint8)
+                ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, _lib._p(packed), _lib._p(depths),
+                                                         len(idxs), int(mode), _lib._p(vals)))
+            else:
+                ctx.check(ctx.lib.ts_score_states(ctx.h, pid, _lib._p(recs) if len(recs) else None,
+                                                  _lib._p(offsets), len(idxs), int(mode),
+                                                  _lib._p(vals)))
         out[np.asarray(idxs)] = vals
     return out
 

@@ -188,3 +188,25 @@ def test_reference_greedy_with_gpu_v_callable(greedy_golden, v0_path):
         g = greedy_golden[key]
         s, visited = ref_greedy(ref_parse(g["text"]), gpu_model_value(params))
         assert [d.render() for d in s.decisions] == g["schedule"] and visited == g["visited"]
+
+
+def test_packed_wire_format_matches(state_sets, v0):
+    """ts_score_states_packed (8-byte decisions + u8 depths) == ts_score_states."""
+    from paper_2011_14486_b200 import _lib
+    z = state_sets["vgg16"]
+    p = pipeline_from(z)
+    states = product_states(p, z["keys"]) * 100
+    ctx = _lib.context(0)
+    ctx.set_params(v0)
+    for inf, idxs, recs, offsets in ss.encode_states(states):
+        pid = ctx.pipeline_id(inf.desc)
+        packed = _lib.pack_records(recs)
+        depths = np.diff(offsets).astype(np.uint8)
+        for mode in (MODE_EXACT, MODE_FAST):
+            a = np.empty(len(idxs))
+            b = np.empty(len(idxs))
+            ctx.check(ctx.lib.ts_score_states(ctx.h, pid, _lib._p(recs), _lib._p(offsets), len(idxs),
+                                              mode, _lib._p(a)))
+            ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, _lib._p(packed), _lib._p(depths),
+                                                     len(idxs), mode, _lib._p(b)))
+            assert np.array_equal(bits(a), bits(b))
