@@ -663,6 +663,15 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
   return fail(ctx, TS_ERR_ARG, "unknown mode");
 }
 
+// Host-path chunking: chunks overlap H2D with scoring; measured on B200
+// (1M VGG-16 states): 4 chunks beat 1 (no overlap) and 8-16 (per-chunk tile
+// tails), so ~n/4 capped at 2^18.
+static int64_t e2e_chunk(int64_t n) {
+  int64_t c = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 18, (n + 3) / 4));
+  if (const char* e = getenv("TS_E2E_CHUNK")) c = std::max<int64_t>(1024, atoll(e));
+  return c;
+}
+
 int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, const int64_t* offsets,
                     int64_t n_states, int mode, double* out_v) {
   if (!ctx || !offsets || !out_v || n_states < 0) return TS_ERR_ARG;
@@ -714,15 +723,6 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, co
   TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   for (auto e : ev) ctx->event_pool.push_back(e);
   return check_device_status(ctx);
-}
-
-// Host-path chunking: chunks overlap H2D with scoring; measured on B200
-// (1M VGG-16 states): 4 chunks beat 1 (no overlap) and 8-16 (per-chunk tile
-// tails), so ~n/4 capped at 2^18.
-static int64_t e2e_chunk(int64_t n) {
-  int64_t c = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 18, (n + 3) / 4));
-  if (const char* e = getenv("TS_E2E_CHUNK")) c = std::max<int64_t>(1024, atoll(e));
-  return c;
 }
 
 // ---- packed wire format (8-byte decisions + u8 depths) for host callers
