@@ -229,7 +229,7 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     S = max(1, args.train_pairs // (T + 1))
     seed0 = 10_000_000 + rank * S
     recs = torch.empty(S * T * 16, dtype=torch.uint8, device=dev)
-    ctx.check(ctx.lib.ts_generate_schedules_device(ctx.h, pid, seed0, S, recs.data_ptr()))
+    ctx.check(ctx.lib.ts_generate_schedules_device(ctx.h, pid, seed0, 1, S, recs.data_ptr()))
     offs = torch.arange(0, (S + 1) * T, T, dtype=torch.int64, device=dev)
     # simulated costs (device cost oracle; host-buffer API, untimed)
     h_recs = recs.cpu().numpy()

@@ -165,8 +165,10 @@ int ts_featurize_rows_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_
 int ts_init_rows(ts_ctx* ctx, int pipeline_id, int normalized, double* out);
 
 /* Complete random schedules (search.random_schedule, search.py:136-142):
- * schedule i uses SearchRng(seed0 + i); records at d_records[i*T .. i*T+T). */
-int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
+ * schedule i starts from splitmix state seed0 + i*stride (stride 1: SearchRng(seed0+i);
+ * stride T*0x9E3779B97F4A7C15: consecutive schedules of one shared SearchRng, each
+ * drawing exactly T times, as learner.bootstrap does); records at d_records[i*T ..). */
+int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, uint64_t stride, int64_t n,
                                  ts_decision* d_records);
 
 /* cost_oracle.benchmark (cost_oracle.py:313-357) for complete schedules:

@@ -107,7 +107,7 @@ def load_library():
             "ts_launch_count": ([vp], i64),
             "ts_set_timing": ([vp, i32], i32),
             "ts_kernel_times": ([vp, vp, vp, i32], i32),
-            "ts_generate_schedules_device": ([vp, i32, ctypes.c_uint64, i64, vp], i32),
+            "ts_generate_schedules_device": ([vp, i32, ctypes.c_uint64, ctypes.c_uint64, i64, vp], i32),
             "ts_benchmark": ([vp, i32, vp, i64, vp, vp, vp, i64, vp], i32),
             "ts_featurize_rows_device": ([vp, i32, vp, vp, i64, vp], i32),
             "ts_init_rows": ([vp, i32, i32, vp], i32),

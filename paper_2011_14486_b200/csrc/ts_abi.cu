@@ -1075,7 +1075,7 @@ int ts_init_rows(ts_ctx* ctx, int pipeline_id, int normalized, double* out) {
   return TS_OK;
 }
 
-int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, int64_t n,
+int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, uint64_t stride, int64_t n,
                                  ts_decision* d_records) {
   if (!ctx || !d_records || n < 0) return TS_ERR_ARG;
   TS_NEED_DEVICE();
@@ -1084,7 +1084,7 @@ int ts_generate_schedules_device(ts_ctx* ctx, int pipeline_id, uint64_t seed0, i
   TS_CUDA(cudaSetDevice(ctx->device));
   TS_CUDA(ctx->tmp.reserve(sizeof(int) * (n > 0 ? n : 1)));
   k_generate<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
-      P->d.as<PipelineDesc>(), seed0, n, d_records, ctx->tmp.as<int>(), ctx->status.as<int>(), 1);
+      P->d.as<PipelineDesc>(), seed0, n, d_records, ctx->tmp.as<int>(), ctx->status.as<int>(), 1, stride);
   TS_LAUNCHED();
   return check_device_status(ctx);
 }

@@ -48,7 +48,7 @@ def test_device_random_schedules_match_reference_walk(costs, gpu_ctx):
         pid = gpu_ctx.pipeline_id(inf.desc)
         n = len(g["states"])
         recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
-        gpu_ctx.check(gpu_ctx.lib.ts_generate_schedules_device(gpu_ctx.h, pid, 1, n, recs.data_ptr()))
+        gpu_ctx.check(gpu_ctx.lib.ts_generate_schedules_device(gpu_ctx.h, pid, 1, 1, n, recs.data_ptr()))
         hr = np.frombuffer(recs.cpu().numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
         for i in range(n):
             dec = [inf.decode(k, r).render() for k, r in enumerate(hr[i * inf.T:(i + 1) * inf.T])]
