@@ -355,7 +355,11 @@ int ts_ctx_create(int device, ts_ctx** out) {
       return TS_ERR_CUDA;
     }
   }
-  const int rc = self_test(ctx);
+  int rc = self_test(ctx);
+  if (!rc) {
+    k_fill_log2_table<<<(LOG2_TABLE + 255) / 256, 256>>>();
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = TS_ERR_CUDA;
+  }
   if (rc) {
     fprintf(stderr, "tensched_b200: %s\n", ctx->err.c_str());
     delete ctx;

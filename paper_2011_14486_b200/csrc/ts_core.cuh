@@ -154,6 +154,22 @@ TS_HD double glibc_log2(double x) {
   return fadd(ffma(r2, p, lo), hi);
 }
 
+// log2 of small integers from a table holding glibc_log2(i) for i < 4096,
+// filled on the device by glibc_log2 itself at context creation (so it is
+// bit-identical by construction); larger arguments compute.  Loop extents,
+// vector widths and 1 + invocations mostly fall in the table.
+constexpr int LOG2_TABLE = 4096;
+#ifdef __CUDACC__
+__device__ double d_log2_int[LOG2_TABLE];
+#endif
+
+TS_HD double log2_int(uint64_t v) {
+#ifdef __CUDA_ARCH__
+  if (v < (uint64_t)LOG2_TABLE) return __ldg(d_log2_int + v);
+#endif
+  return glibc_log2((double)v);
+}
+
 // ------------------------------------------------------------ 256-bit ints
 // Invocation counts reach 133 bits on random VGG-16 states (inv*ppi 141,
 // SURVEY.md 7 hard part 4); 256 bits with an overflow status.  All limb
@@ -593,9 +609,9 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
   for (int j = 0; j < TS_MAX_LOOPS; ++j)
     if (j == n.n_loops - 1) inner = n.ext[j];
   f[0] = 1.0;
-  f[1] = glibc_log2((double)d.vec);
-  f[2] = (d.flags & TS_FLAG_PARALLEL) ? glibc_log2((double)n.ext[0]) : 0.0;
-  f[3] = glibc_log2((double)inner);
+  f[1] = log2_int(d.vec);
+  f[2] = (d.flags & TS_FLAG_PARALLEL) ? log2_int(n.ext[0]) : 0.0;
+  f[3] = log2_int(inner);
   f[4] = (double)n.depth;
   // recompute factor = Fraction(inv * ppi, domain_points)  (cost_oracle.py:108-121)
   uint64_t region = 1;
@@ -628,7 +644,7 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
   f[6] = pts <= 8192u ? 1.0 : 0.0;  // 4 * pts <= 32768, overflow-free
   u256 inv1 = n.inv;
   if (!u256_add_u64(inv1, 1)) return TS_ERR_OVERFLOW;
-  f[7] = glibc_log2(u256_to_double(inv1));
+  f[7] = u256_small(inv1) ? log2_int(inv1.w[0]) : glibc_log2(u256_to_double(inv1));
   return TS_OK;
 }
 
