@@ -370,6 +370,55 @@ TS_HD_NOINLINE double u256_div_to_double_slow(const u256& n, const Divisor& D) {
   return round_u256(q, inexact, -k);
 }
 
+// a * m with overflow detection past 128 bits
+TS_HD unsigned __int128 mul128_64(unsigned __int128 a, uint64_t m, bool& ok) {
+  const unsigned __int128 lo = (unsigned __int128)(uint64_t)a * m;
+  const unsigned __int128 hi = (unsigned __int128)(uint64_t)(a >> 64) * m;
+  ok = ok && (hi >> 64) == 0;
+  const unsigned __int128 r = lo + (hi << 64);
+  ok = ok && r >= lo;
+  return r;
+}
+
+TS_HD int bitlen128(unsigned __int128 a) {
+  const uint64_t hi = (uint64_t)(a >> 64);
+  return hi ? 128 - clz64(hi) : 64 - clz64((uint64_t)a);
+}
+
+// q (>= 55 bits) + fraction (sticky) rounded half-even to 53 bits, * 2^e2
+TS_HD double round_u64(uint64_t q, bool sticky, int e2) {
+  const int sh = 64 - clz64(q) - 53;
+  uint64_t mant = q >> sh;
+  const bool half = (q >> (sh - 1)) & 1ull;
+  const bool below = sticky || (q & ((1ull << (sh - 1)) - 1)) != 0;
+  if (half && (below || (mant & 1ull))) mant += 1;
+  return make_double(mant, e2 + sh);
+}
+
+// Correctly rounded n / d for n < 2^128 (long_true_divide semantics): scale
+// so the integer quotient carries 55-56 bits, one 128/64 division with the
+// divisor's precomputed reciprocal, then half-even rounding with sticky.
+TS_HD double div128_to_double(unsigned __int128 n, const Divisor& D) {
+  if (n == 0) return 0.0;
+  const int a = bitlen128(n);
+  const int b = 64 - clz64(D.d);
+  int k = 55 + b - a;
+  unsigned __int128 N;
+  bool sticky = false;
+  if (k >= 0) {
+    N = n << k;  // < 2^(55+b) <= 2^119
+  } else {
+    const int j = -k;
+    N = n >> j;
+    sticky = (n & (((unsigned __int128)1 << j) - 1)) != 0;
+  }
+  // N < d * 2^56, so N << shift fits 128 bits and the quotient fits 64
+  const unsigned __int128 Nn = N << D.shift;
+  uint64_t r;
+  const uint64_t q = div2by1((uint64_t)(Nn >> 64), (uint64_t)Nn, D.dn, D.inv, r);
+  return round_u64(q, sticky || r != 0, -k);
+}
+
 TS_HD double u256_div_to_double(const u256& n, const Divisor& D) {
   if (u256_small(n) && n.w[0] <= (1ull << 53) && D.d <= (1ull << 53))
     return fdiv(u64_to_double(n.w[0]), u64_to_double(D.d));  // both exact: IEEE division
@@ -618,20 +667,16 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
 #pragma unroll
   for (int k = 0; k < TS_MAX_PURE; ++k)
     if (k < s.n_pure) region *= (uint64_t)pe[k];
-  bool fast = u256_small(n.inv);
-  uint64_t p = n.inv.w[0];
-#ifdef __CUDA_ARCH__
-  fast = fast && __umul64hi(p, region) == 0;
-  p *= region;
-  fast = fast && __umul64hi(p, s.red_points) == 0;
-#else
-  fast = fast && ((unsigned __int128)p * region) >> 64 == 0;
-  p *= region;
-  fast = fast && ((unsigned __int128)p * s.red_points) >> 64 == 0;
-#endif
-  p *= s.red_points;
-  if (fast && p <= (1ull << 53) && s.dp.d <= (1ull << 53)) {
-    f[5] = glibc_log2(fdiv(u64_to_double(p), u64_to_double(s.dp.d)));  // both exact
+  // inv * ppi below 2^128 (all but the deepest anchor chains): one
+  // branch-uniform 128-bit correctly rounded division
+  bool fit = n.inv.w[2] == 0 && n.inv.w[3] == 0;
+  unsigned __int128 num128 = 0;
+  if (fit) {
+    num128 = mul128_64(((unsigned __int128)n.inv.w[1] << 64) | n.inv.w[0], region, fit);
+    num128 = mul128_64(num128, s.red_points, fit);
+  }
+  if (fit) {
+    f[5] = glibc_log2(div128_to_double(num128, s.dp));
   } else {
     u256 num = n.inv;
     bool ok = u256_mul_u64(num, region);

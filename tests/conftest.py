@@ -76,6 +76,8 @@ def native_core():
     lib.core_to_double.restype = ctypes.c_double
     lib.core_to_double.argtypes = [vp]
     lib.core_featurize.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_int64, vp]
+    lib.core_div128.restype = ctypes.c_double
+    lib.core_div128.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
     return lib
 
 

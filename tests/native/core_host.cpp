@@ -74,3 +74,7 @@ extern "C" double core_to_double(const uint64_t* n4) {
   for (int i = 0; i < 4; ++i) a.w[i] = n4[i];
   return u256_to_double(a);
 }
+
+extern "C" double core_div128(uint64_t lo, uint64_t hi, uint64_t d) {
+  return div128_to_double(((unsigned __int128)hi << 64) | lo, make_divisor(d));
+}

@@ -129,6 +129,23 @@ def test_native_core_bigint_rounding(native_core):
         assert native_core.core_to_double(limbs(tie).ctypes.data) == float(tie)
 
 
+def test_native_core_div128_correctly_rounded(native_core):
+    """The 128-bit division path of the recompute feature equals CPython's
+    int/int true division, including exact halfway cases."""
+    rng = random.Random(11)
+    M = (1 << 64) - 1
+    for _ in range(100000):
+        n = rng.getrandbits(rng.randint(1, 127)) + 1
+        d = rng.getrandbits(rng.randint(1, 63)) + 1
+        assert native_core.core_div128(n & M, n >> 64, d) == n / d, (n, d)
+    for _ in range(20000):  # ties: n/d = (odd 54-bit) / 2 * 2^e
+        d = rng.getrandbits(rng.randint(1, 40)) + 1
+        q = ((rng.getrandbits(52) | (1 << 52)) * 2 + 1)
+        n = q * d << rng.randint(0, 10)
+        if n < (1 << 127):
+            assert native_core.core_div128(n & M, n >> 64, d * 2) == n / (d * 2)
+
+
 def test_native_core_features_bit_exact(state_sets, native_core):
     for name, z in state_sets.items():
         p = pipeline_from(z)
