@@ -689,7 +689,16 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
   f[6] = pts <= 8192u ? 1.0 : 0.0;  // 4 * pts <= 32768, overflow-free
   u256 inv1 = n.inv;
   if (!u256_add_u64(inv1, 1)) return TS_ERR_OVERFLOW;
-  f[7] = u256_small(inv1) ? log2_int(inv1.w[0]) : glibc_log2(u256_to_double(inv1));
+  if (u256_small(inv1)) {
+    f[7] = log2_int(inv1.w[0]);
+  } else if (inv1.w[2] == 0 && inv1.w[3] == 0) {  // < 2^128: top 64 bits + sticky
+    const int sh = 64 - clz64(inv1.w[1]);
+    const uint64_t top = (inv1.w[1] << (64 - sh)) | (sh < 64 ? inv1.w[0] >> sh : 0);
+    const bool sticky = sh < 64 ? (inv1.w[0] & ((1ull << sh) - 1)) != 0 : inv1.w[0] != 0;
+    f[7] = glibc_log2(round_u64(top, sticky, sh));
+  } else {
+    f[7] = glibc_log2(u256_to_double(inv1));
+  }
   return TS_OK;
 }
 

@@ -78,6 +78,8 @@ def native_core():
     lib.core_featurize.argtypes = [vp, ctypes.c_int64, vp, vp, ctypes.c_int64, vp]
     lib.core_div128.restype = ctypes.c_double
     lib.core_div128.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+    lib.core_log2_1p.restype = ctypes.c_double
+    lib.core_log2_1p.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
     return lib
 
 

@@ -78,3 +78,28 @@ extern "C" double core_to_double(const uint64_t* n4) {
 extern "C" double core_div128(uint64_t lo, uint64_t hi, uint64_t d) {
   return div128_to_double(((unsigned __int128)hi << 64) | lo, make_divisor(d));
 }
+
+// f15 = log2(1 + inv) through acquired_features' conversion paths
+extern "C" double core_log2_1p(uint64_t lo, uint64_t hi) {
+  StageDesc s;
+  memset(&s, 0, sizeof s);
+  s.n_pure = 1;
+  s.ext[0] = 1;
+  s.pure_points = 1;
+  s.red_points = 1;
+  s.domain_points = 1;
+  s.dp = make_divisor(1);
+  Nest n;
+  memset(&n, 0, sizeof n);
+  n.inv.w[0] = lo;
+  n.inv.w[1] = hi;
+  n.n_loops = 1;
+  n.ext[0] = 1;
+  ts_decision d;
+  memset(&d, 0, sizeof d);
+  d.vec = 1;
+  int64_t pe[4] = {1, 1, 1, 1};
+  double f[8];
+  if (acquired_features(s, n, pe, d, f)) return -1.0;
+  return f[7];
+}

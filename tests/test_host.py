@@ -146,6 +146,19 @@ def test_native_core_div128_correctly_rounded(native_core):
             assert native_core.core_div128(n & M, n >> 64, d * 2) == n / (d * 2)
 
 
+def test_native_core_log2_1p_invocations(native_core):
+    """f15 = log2(1 + inv) (PyLong_AsDouble then libm log2) for invocation
+    counts across 64-, 128- and 256-bit paths."""
+    rng = random.Random(5)
+    M = (1 << 64) - 1
+    for _ in range(20000):
+        inv = rng.getrandbits(rng.randint(1, 127))
+        assert native_core.core_log2_1p(inv & M, inv >> 64) == math.log2(1 + inv), inv
+    for hi_bits in range(1, 65):  # exact boundaries of the top-64 extraction
+        inv = (1 << (63 + hi_bits)) - 1
+        assert native_core.core_log2_1p(inv & M, inv >> 64) == math.log2(1 + inv)
+
+
 def test_native_core_features_bit_exact(state_sets, native_core):
     for name, z in state_sets.items():
         p = pipeline_from(z)
