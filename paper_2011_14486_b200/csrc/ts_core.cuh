@@ -491,24 +491,19 @@ TS_HD bool anchor_ok(const Nest& c, int lvl) {
 TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& cn, int lvl,
                            int64_t* pe, u256& inv, int& depth) {
   // invocations = consumer invocations * prod(outer loop extents up to lvl);
-  // a 64-bit fast path covers the common case, 256 bits the deep chains
+  // a 128-bit path covers all but the deepest chains (branch-uniform within
+  // a warp far more often than a 64/256 split), 256 bits the rest
   bool ok = true;
   {
-    uint64_t p = cn.inv.w[0];
-    bool small = u256_small(cn.inv);
+    unsigned __int128 p = ((unsigned __int128)cn.inv.w[1] << 64) | cn.inv.w[0];
+    bool fit = cn.inv.w[2] == 0 && cn.inv.w[3] == 0;
 #pragma unroll
-    for (int j = 0; j < TS_MAX_LOOPS; ++j) {
-      if (j <= lvl && j < cn.n_loops) {
-#ifdef __CUDA_ARCH__
-        small = small && __umul64hi(p, cn.ext[j]) == 0;
-#else
-        small = small && ((unsigned __int128)p * cn.ext[j]) >> 64 == 0;
-#endif
-        p *= cn.ext[j];
-      }
-    }
-    if (small) {
-      inv = u256_from(p);
+    for (int j = 0; j < TS_MAX_LOOPS; ++j)
+      if (j <= lvl && j < cn.n_loops) p = mul128_64(p, cn.ext[j], fit);
+    if (fit) {
+      inv.w[0] = (uint64_t)p;
+      inv.w[1] = (uint64_t)(p >> 64);
+      inv.w[2] = inv.w[3] = 0;
     } else {
       inv = cn.inv;
 #pragma unroll
