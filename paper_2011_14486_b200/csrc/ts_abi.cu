@@ -617,8 +617,9 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     rc = ensure_fast_prefix(ctx, P);
     if (rc) return rc;
     // bucket states by depth (descending) so tiles share their depth
-    TS_CUDA(ctx->reps.reserve(sizeof(int) * (n_states + 2 * (T + 2))));
-    int* perm = ctx->reps.as<int>();
+    TS_CUDA(ctx->reps.reserve(sizeof(int64_t) * (T + 2) + sizeof(int) * (n_states + 2 * (T + 2))));
+    int64_t* rowoff = ctx->reps.as<int64_t>();
+    int* perm = reinterpret_cast<int*>(rowoff + (T + 2));
     int* hist = perm + n_states;
     int* cursor = hist + (T + 2);
     const unsigned g = (unsigned)((n_states + 255) / 256);
@@ -628,7 +629,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       tc::k_depth_hist<<<std::min<unsigned>(g, 4u * ctx->sm_count), 256, sizeof(int) * (T + 1), ctx->stream>>>(
           d_offsets, n_states, T, hist);
       TS_LAUNCHED();
-      tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor);
+      tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor, rowoff);
       TS_LAUNCHED();
       tc::k_depth_scatter<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, cursor, perm);
       TS_LAUNCHED();
@@ -639,7 +640,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>(),
-          perm);
+          perm, rowoff);
       TS_LAUNCHED();
     }
     tc::TcArgs ta;
@@ -648,6 +649,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     ta.rows32 = ctx->rows.as<float>();
     ta.offsets = d_offsets;
     ta.perm = perm;
+    ta.rowoff = rowoff;
     ta.pre = P->pre_fast.as<float>();
     ta.out = d_out;
     ta.n = n_states;

@@ -209,6 +209,7 @@ struct TcArgs {
   const float* rows32;      // [n_records][16] normalized scheduled rows (fp32)
   const int64_t* offsets;   // [n+1]
   const int* perm;          // [n] sorted position -> state
+  const int64_t* rowoff;    // [T+1] decision-major row offsets (k_depth_scan)
   float* pre;               // [(T+1)][PRE_STRIDE] fast prefix (h, c, raw)
   double* out;              // [n] V
   int64_t n;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       for (int g8 = 0; g8 < 4; ++g8) put_h8(A, r, g8, h0 + 8 * g8);
     }
     float x[16];
-    load_x((t0 < T - d) ? a.init32 + t0 * 16 : a.rows32 + (off + (T - 1 - t0)) * 16, x);
+    load_x((t0 < T - d) ? a.init32 + t0 * 16 : a.rows32 + (a.rowoff[T - 1 - t0] + sp) * 16, x);
     for (int t = t0; t < T; ++t) {
       put_x(A, r, x);
       fence_async_smem();
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       }
       // prefetch the next row while the tensor core works
       if (t + 1 < T)
-        load_x((t + 1 < T - d) ? a.init32 + (t + 1) * 16 : a.rows32 + (off + (T - 2 - t)) * 16, x);
+        load_x((t + 1 < T - d) ? a.init32 + (t + 1) * 16 : a.rows32 + (a.rowoff[T - 2 - t] + sp) * 16, x);
       mbar_wait(bar, phase);
       phase ^= 1u;
       fence_after();
@@ -412,13 +413,25 @@ __global__ void k_depth_hist(const int64_t* __restrict__ offsets, int64_t n, int
 }
 
 // descending depth: cursor[d] = number of states with depth > d
-__global__ void k_depth_scan(const int* __restrict__ hist, int T, int* __restrict__ cursor) {
+// rowoff[i] = first row of decision i in the depth-sorted, decision-major
+// row layout: decision i of the state at sorted position p lives at
+// rowoff[i] + p (only states deeper than i have one), so consecutive sorted
+// positions - a warp of the featurizer, a tile of the LSTM - touch
+// consecutive rows.
+__global__ void k_depth_scan(const int* __restrict__ hist, int T, int* __restrict__ cursor,
+                             int64_t* __restrict__ rowoff) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     int acc = 0;
     for (int d = T; d >= 0; --d) {
       cursor[d] = acc;
       acc += hist[d];
     }
+    int64_t r = 0;
+    for (int i = 0; i < T; ++i) {
+      rowoff[i] = r;
+      r += cursor[i];  // states with depth > i
+    }
+    rowoff[T] = r;
   }
 }
 
