@@ -1290,14 +1290,30 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
   a.dz = ctx->tr_dz.as<double>();
   a.target_scale = target_scale;
   a.n_total = (double)n_total;
-  tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
-  TS_LAUNCHED();
   const int64_t K = (int64_t)ctx->tr_Tmax * B;
-  const int ksplit = (int)std::min<int64_t>(64, std::max<int64_t>(1, K / 512));
-  TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
-  tr::k_train_wgrad<<<dim3((L.n + 255) / 256, ksplit), 256, 0, ctx->stream>>>(a, ksplit,
-                                                                             ctx->tr_partial.as<double>());
-  TS_LAUNCHED();
+  int ksplit;
+  if (ctx->tr_H == tr::GH && !getenv("TS_TRAIN_WARP")) {
+    // grouped kernels (bit-identical forward/BPTT; weight gradients in the
+    // same pair order within each of ksplit ranges)
+    TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(tr::GroupSmem)));
+    tr::k_train_fb_group<<<(unsigned)((B + tr::GS - 1) / tr::GS), tr::GTHREADS, sizeof(tr::GroupSmem),
+                           ctx->stream>>>(a);
+    TS_LAUNCHED();
+    ksplit = (int)std::min<int64_t>(2 * ctx->sm_count, std::max<int64_t>(1, K / 64));
+    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
+    tr::k_train_wgrad_group<<<ksplit, tr::GTHREADS, sizeof(tr::WgradSmem), ctx->stream>>>(
+        a, ksplit, ctx->tr_partial.as<double>());
+    TS_LAUNCHED();
+  } else {
+    tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
+    TS_LAUNCHED();
+    ksplit = (int)std::min<int64_t>(64, std::max<int64_t>(1, K / 512));
+    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
+    tr::k_train_wgrad<<<dim3((L.n + 255) / 256, ksplit), 256, 0, ctx->stream>>>(a, ksplit,
+                                                                               ctx->tr_partial.as<double>());
+    TS_LAUNCHED();
+  }
   tr::k_train_reduce<<<(L.n + 255) / 256, 256, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
   TS_LAUNCHED();
   if (raw_out) {

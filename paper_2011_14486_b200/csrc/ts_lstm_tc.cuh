@@ -149,6 +149,26 @@ __device__ __forceinline__ float ex2_sel(float x, int slot) {
   return slot < TS_FMA_EXP ? ex2_fma(x) : ex2(x);
 }
 
+// 1/d on the FMA pipe for d in [1, 2^126): integer seed (|rel err| < 1/8)
+// and two cubic Newton steps r += r*(e + e^2), e = 1 - d*r (error ~1e-9
+// before rounding, i.e. within 1-2 ulp like rcp.approx).
+__device__ __forceinline__ float rcp_fma(float d) {
+  float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const float e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, fmaf(e, e, e), r);
+  }
+  return r;
+}
+
+#ifndef TS_FMA_RCP
+#define TS_FMA_RCP 0  // how many of the 2 per-unit reciprocals use rcp_fma (0..2)
+#endif
+__device__ __forceinline__ float rcp_sel(float x, int slot) {
+  return slot < TS_FMA_RCP ? rcp_fma(x) : rcp(x);
+}
+
 // hi/lo fp16 split of 8 floats into two 16-byte chunks
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
@@ -356,9 +376,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           const float ti = 1.0f + ei, tf = 1.0f + ef, tg = 1.0f + eg;
           const float tig = ti * tg;
           const float num = fmaf(c[j], tig, (1.0f - eg) * tf);
-          c[j] = num * rcp(tf * tig);
+          c[j] = num * rcp_sel(tf * tig, 0);
           const float ec = ex2_sel(clamp40(c2 * c[j]), 4);
-          h8[u] = (1.0f - ec) * rcp((1.0f + eo) * (1.0f + ec));
+          h8[u] = (1.0f - ec) * rcp_sel((1.0f + eo) * (1.0f + ec), 1);
           acc = fmaf(h8[u], wout[j], acc);
         }
         // the UMMA that read A has completed (mbarrier), so h can go straight in

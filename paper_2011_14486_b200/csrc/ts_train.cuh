@@ -249,6 +249,266 @@ __global__ void k_train_apply(double* __restrict__ P, const double* __restrict__
   if (threadIdx.x == 0 && norm_out) *norm_out = norm;
 }
 
+// ------------------------------------------------ H = 32: sequence groups
+// The warp-per-sequence kernels above are latency-bound (one dependent fp64
+// chain per lane, weights re-read through L1 every timestep).  For the
+// model's H = 32 the batch is instead processed in groups of GS sequences per
+// CTA with the weights resident in shared memory: every timestep is a small
+// [GS x 48] x [48 x 128] product (thread = gate column, 8 sequences each) and
+// the BPTT step a [GS x 128] x [128 x 32] product (thread = hidden unit, 2
+// sequences), so each thread carries 8 (resp. 2) independent chains.  Every
+// output keeps the warp kernels' summation order and non-fused mul/add, so
+// the results are bit-identical to k_train_fb (tested).
+constexpr int GS = 16;
+constexpr int GTHREADS = 256;
+constexpr int GH = 32, GG = 128, GK = 48;
+
+struct GroupSmem {
+  double W[GK][GG];    // rows 0..15 Wx, 16..47 Wh (the flat parameter order)
+  double WhT[GG][GH];  // Wh transposed for dh_next
+  double xh[GS][GK];   // [x_t | h_{t-1}] per sequence
+  double zb[GS][GG];   // gate pre-activations (forward), dz (backward)
+  double b[GG];
+  double w[GH];
+};
+
+__global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
+  extern __shared__ __align__(16) double tr_dyn_smem[];
+  GroupSmem& S = *reinterpret_cast<GroupSmem*>(tr_dyn_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Layout L(GH);
+  const double* P = a.P;
+  for (int e = tid; e < GK * GG; e += GTHREADS) (&S.W[0][0])[e] = P[L.oWx + e];
+  for (int e = tid; e < GH * GG; e += GTHREADS) S.WhT[e % GG][e / GG] = P[L.oWh + e];
+  for (int e = tid; e < GG; e += GTHREADS) S.b[e] = P[L.ob + e];
+  if (tid < GH) S.w[tid] = P[L.ow + tid];
+  for (int e = tid; e < GS * GK; e += GTHREADS) (&S.xh[0][0])[e] = 0.0;
+  const int g0 = blockIdx.x * GS;
+  int Tg = 0;
+  for (int s = 0; s < GS; ++s)
+    if (g0 + s < a.B) Tg = max(Tg, a.D.Tlen[a.batch[g0 + s]]);
+  // gate-phase ownership: sequence s = warp + 8q, hidden unit j = lane
+  int idx[2], Tq[2];
+  double raw[2], c[2] = {0.0, 0.0};
+  double* cache[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int b = g0 + warp + 8 * q;
+    const bool v = b < a.B;
+    idx[q] = v ? a.batch[b] : 0;
+    Tq[q] = v ? a.D.Tlen[idx[q]] : 0;
+    raw[q] = fmul((double)Tq[q], P[L.obout]);
+    cache[q] = a.cache + (int64_t)(v ? b : 0) * a.Tmax * CACHE_FIELDS * GH;
+  }
+  __syncthreads();
+  // ---- forward with cache
+  for (int t = 0; t < Tg; ++t) {
+    {  // x rows: one feature per thread
+      const int s = tid >> 4, k = tid & 15, b = g0 + s;
+      double v = 0.0;
+      if (b < a.B) {
+        const int i = a.batch[b];
+        if (t < a.D.Tlen[i]) v = a.D.x(i, t)[k];
+      }
+      S.xh[s][k] = v;
+    }
+    __syncthreads();
+    {  // z = b + x Wx + h Wh, column n for sequences s0, s0+2, ..
+      const int n = tid & (GG - 1), s0 = tid >> 7;
+      double z[8];
+      const double bn = S.b[n];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z[i] = bn;
+#pragma unroll 4
+      for (int k = 0; k < GK; ++k) {
+        const double wk = S.W[k][n];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) z[i] = fadd(z[i], fmul(S.xh[s0 + 2 * i][k], wk));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) S.zb[s0 + 2 * i][n] = z[i];
+    }
+    __syncthreads();
+    double hn[2] = {0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int s = warp + 8 * q;
+      if (t >= Tq[q]) continue;  // warp-uniform
+      const double gi = sig(S.zb[s][lane]), gf = sig(S.zb[s][GH + lane]), gg = tanh(S.zb[s][2 * GH + lane]),
+                   go = sig(S.zb[s][3 * GH + lane]);
+      const double c_prev = c[q], h_prev = S.xh[s][16 + lane];
+      c[q] = fadd(fmul(gf, c[q]), fmul(gi, gg));
+      const double tc = tanh(c[q]);
+      const double h = fmul(go, tc);
+      double* cc = cache[q] + (int64_t)t * CACHE_FIELDS * GH;
+      cc[0 * GH + lane] = gi;
+      cc[1 * GH + lane] = gf;
+      cc[2 * GH + lane] = gg;
+      cc[3 * GH + lane] = go;
+      cc[4 * GH + lane] = c_prev;
+      cc[5 * GH + lane] = h_prev;
+      cc[6 * GH + lane] = tc;
+      cc[7 * GH + lane] = h;
+      hn[q] = h;
+      const double prod = fmul(h, S.w[lane]);
+      double acc = 0.0;
+      for (int k = 0; k < GH; ++k) acc = fadd(acc, __shfl_sync(0xffffffffu, prod, k));
+      raw[q] = fadd(raw[q], acc);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (t < Tq[q]) S.xh[warp + 8 * q][16 + lane] = hn[q];
+  }
+  // d_raw = 2 (raw + ts - log t) / n  (value_model.py:201)
+  double d_raw[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int b = g0 + warp + 8 * q;
+    d_raw[q] = 0.0;
+    if (b >= a.B) continue;
+    d_raw[q] = fdiv(fmul(2.0, fsub(fadd(raw[q], a.target_scale), a.D.logt[idx[q]])), a.n_total);
+    if (lane == 0) {
+      a.raw[b] = raw[q];
+      a.draw[b] = d_raw[q];
+    }
+  }
+  // ---- BPTT
+  double dh_next[2] = {0.0, 0.0}, dc_next[2] = {0.0, 0.0};
+  const double wj = S.w[lane];
+  for (int t = Tg - 1; t >= 0; --t) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (t >= Tq[q]) continue;
+      const int s = warp + 8 * q, b = g0 + s;
+      const double* cc = cache[q] + (int64_t)t * CACHE_FIELDS * GH;
+      const double gi = cc[lane], gf = cc[GH + lane], gg = cc[2 * GH + lane], go = cc[3 * GH + lane];
+      const double c_prev = cc[4 * GH + lane], tc = cc[6 * GH + lane];
+      const double dh = fadd(fmul(wj, d_raw[q]), dh_next[q]);
+      const double d_o = fmul(dh, tc);
+      const double dc = fadd(dc_next[q], fmul(fmul(dh, go), fsub(1.0, fmul(tc, tc))));
+      const double di = fmul(dc, gg), df = fmul(dc, c_prev), dg = fmul(dc, gi);
+      dc_next[q] = fmul(dc, gf);
+      const double dzi = fmul(fmul(di, gi), fsub(1.0, gi));
+      const double dzf = fmul(fmul(df, gf), fsub(1.0, gf));
+      const double dzg = fmul(dg, fsub(1.0, fmul(gg, gg)));
+      const double dzo = fmul(fmul(d_o, go), fsub(1.0, go));
+      double* dzt = a.dz + ((int64_t)b * a.Tmax + t) * GG;
+      dzt[lane] = dzi;
+      dzt[GH + lane] = dzf;
+      dzt[2 * GH + lane] = dzg;
+      dzt[3 * GH + lane] = dzo;
+      S.zb[s][lane] = dzi;
+      S.zb[s][GH + lane] = dzf;
+      S.zb[s][2 * GH + lane] = dzg;
+      S.zb[s][3 * GH + lane] = dzo;
+    }
+    __syncthreads();
+    // dh_next = dz @ Wh.T in gate-column order
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (t >= Tq[q]) continue;
+      const int s = warp + 8 * q;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int col = 0; col < GG; ++col) acc = fadd(acc, fmul(S.zb[s][col], S.WhT[col][lane]));
+      dh_next[q] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Weight gradients, H = 32: one CTA per k-split range of the (t descending,
+// b) pair sequence, all 6,305 parameters per CTA.  Chunks of WCH pairs are
+// staged in shared memory ([x | h_prev], dz, h, d_raw); thread (rg, cg) owns
+// the 3 x 8 block rows rg + 16i, columns cg + 16j of [dWx; dWh], threads
+// 0..127 also db, 128..159 dw, 160 db_out.  Each parameter is accumulated in
+// pair order with non-fused mul/add, as in k_train_wgrad.
+constexpr int WCH = 16;
+struct WgradSmem {
+  double A[WCH][GK];
+  double D[WCH][GG];
+  double Hh[WCH][GH];
+  double dr[WCH];
+  double tdr[WCH];     // T * d_raw (db_out term, rows with t == 0)
+  int valid[WCH];
+  int first[WCH];      // t == 0
+};
+
+__global__ void __launch_bounds__(GTHREADS) k_train_wgrad_group(TrainArgs a, int ksplit,
+                                                                double* __restrict__ partial) {
+  extern __shared__ __align__(16) double tr_dyn_smem[];
+  WgradSmem& S = *reinterpret_cast<WgradSmem*>(tr_dyn_smem);
+  const Layout L(GH);
+  const int tid = threadIdx.x;
+  const int rg = tid >> 4, cg = tid & 15;
+  const int64_t K = (int64_t)a.Tmax * a.B;
+  const int64_t k0 = K * blockIdx.x / ksplit, k1 = K * (blockIdx.x + 1) / ksplit;
+  double acc[3][8];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  double extra = 0.0;
+  for (int64_t kb = k0; kb < k1; kb += WCH) {
+    const int nk = (int)(k1 - kb < WCH ? k1 - kb : WCH);
+    __syncthreads();  // previous chunk consumed
+    if (tid < nk) {
+      const int64_t kk = kb + tid;
+      const int t = a.Tmax - 1 - (int)(kk / a.B);
+      const int b = (int)(kk % a.B);
+      const int T = a.D.Tlen[a.batch[b]];
+      S.valid[tid] = t < T;
+      S.first[tid] = t == 0;
+      S.dr[tid] = a.draw[b];
+      S.tdr[tid] = fmul((double)T, a.draw[b]);
+    }
+    __syncthreads();
+    // stage rows: 16 x, 32 h_prev, 32 h, 128 dz per pair
+    for (int e = tid; e < nk * 208; e += GTHREADS) {
+      const int rr = e / 208, f = e % 208;
+      if (!S.valid[rr]) continue;
+      const int64_t kk = kb + rr;
+      const int t = a.Tmax - 1 - (int)(kk / a.B);
+      const int b = (int)(kk % a.B);
+      const int64_t bt = (int64_t)b * a.Tmax + t;
+      if (f < 16) {
+        S.A[rr][f] = a.D.x(a.batch[b], t)[f];
+      } else if (f < 48) {
+        S.A[rr][f] = a.cache[(bt * CACHE_FIELDS + 5) * GH + (f - 16)];
+      } else if (f < 80) {
+        S.Hh[rr][f - 48] = a.cache[(bt * CACHE_FIELDS + 7) * GH + (f - 48)];
+      } else {
+        S.D[rr][f - 80] = a.dz[bt * GG + (f - 80)];
+      }
+    }
+    __syncthreads();
+    for (int rr = 0; rr < nk; ++rr) {
+      if (tid == 160 && S.first[rr]) extra = fadd(extra, S.tdr[rr]);
+      if (!S.valid[rr]) continue;  // uniform
+      double av[3], dv[8];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) av[i] = S.A[rr][rg + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dv[j] = S.D[rr][cg + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fadd(acc[i][j], fmul(av[i], dv[j]));
+      if (tid < GG) extra = fadd(extra, S.D[rr][tid]);
+      else if (tid < GG + GH) extra = fadd(extra, fmul(S.Hh[rr][tid - GG], S.dr[rr]));
+    }
+  }
+  double* out = partial + (int64_t)blockIdx.x * L.n;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[(rg + 16 * i) * GG + cg + 16 * j] = acc[i][j];
+  if (tid < GG) out[L.ob + tid] = extra;
+  else if (tid < GG + GH) out[L.ow + tid - GG] = extra;
+  else if (tid == GG + GH) out[L.obout] = extra;
+}
+
 // raw for a list of sequences (eval, Cython order with the zero skip):
 // warp per sequence
 __global__ void k_train_fwd(TrainArgs a) {

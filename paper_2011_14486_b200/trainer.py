@@ -97,11 +97,13 @@ class DeviceGradients:
         self.ctx.check(self.ctx.lib.ts_train_get_params(self.ctx.h, _lib._p(out), out.size))
         return out
 
-    def grads(self, idx, n_total, target_scale, d_grad_ptr=None):
+    def grads(self, idx, n_total, target_scale, d_grad_ptr=None, raw_out=None):
+        """raw_out: optional f64[len(idx)] host array receiving the forward raw."""
         idx = np.ascontiguousarray(idx, dtype=np.int32)
         self.ctx.check(self.ctx.lib.ts_train_grads(
             self.ctx.h, _lib._p(idx), len(idx), int(n_total), float(target_scale),
-            ctypes.c_void_p(d_grad_ptr) if d_grad_ptr else None, None))
+            ctypes.c_void_p(d_grad_ptr) if d_grad_ptr else None,
+            _lib._p(raw_out) if raw_out is not None else None))
 
     def apply(self, lr, clip, d_grad_ptr=None):
         self.ctx.check(self.ctx.lib.ts_train_apply(

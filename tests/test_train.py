@@ -115,6 +115,46 @@ def test_device_gradients_match_oracle(golden, v0_path):
 
 
 @pytest.mark.gpu
+def test_grouped_kernels_match_warp_kernels(golden, v0_path, monkeypatch):
+    """The H = 32 grouped forward/BPTT kernel is bit-identical to the
+    warp-per-sequence kernel (same summation orders); the grouped weight
+    gradients differ only in the k-split boundaries (<= 1e-12 relative).
+    Ragged lengths, a batch that is not a multiple of the group size, and
+    repeated indices."""
+    import torch
+    from paper_2011_14486_b200 import _lib
+    from paper_2011_14486_b200.featurizer import featurize_states, normalize
+    from paper_2011_14486_b200.trainer import DeviceGradients, flat_params
+    from paper_2011_14486_b200.value_model import load
+    g, data = _dataset(golden)
+    params = load(v0_path)
+    mats = featurize_states([s for s, _ in data])
+    T = np.array([m.shape[0] for m in mats], dtype=np.int32)
+    X = np.zeros((len(mats), T.max(), 16))
+    for i, m in enumerate(mats):
+        X[i, : len(m)] = normalize(params.normalizer, m)
+    logt = np.log([t for _, t in data])
+    dev = DeviceGradients(_lib.context(0), X, T, logt, params.hidden)
+    dev.set_params(flat_params(params))
+    rng = np.random.default_rng(7)
+    for B in (1, 37, 600):
+        batch = rng.integers(0, len(mats), size=B).astype(np.int32)
+        out = {}
+        for mode in ("group", "warp"):
+            if mode == "warp":
+                monkeypatch.setenv("TS_TRAIN_WARP", "1")
+            else:
+                monkeypatch.delenv("TS_TRAIN_WARP", raising=False)
+            gb = torch.zeros(dev.n_params, dtype=torch.float64, device="cuda")
+            raw = np.zeros(B)
+            dev.grads(batch, B, params.target_scale, gb.data_ptr(), raw_out=raw)
+            dev.sync()
+            out[mode] = (raw, gb.cpu().numpy())
+        assert np.array_equal(out["group"][0], out["warp"][0])
+        np.testing.assert_allclose(out["group"][1], out["warp"][1], rtol=1e-12, atol=1e-17)
+
+
+@pytest.mark.gpu
 def test_device_training_reproduces_reference_v0(golden, v0_path):
     """`tensched train <train assets> --rounds 0 --seed 0` on the device:
     same PCG64 split/permutations, final V within 1e-4 of the reference's
