@@ -119,7 +119,8 @@ struct ts_ctx {
   // V training (ts_train_*)
   int tr_H = 0, tr_Tmax = 0;
   int64_t tr_N = 0;
-  DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm, tr_partial;
+  DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm, tr_partial,
+      tr_pvalid;
   tr::Data tr_data{};
 };
 
@@ -1256,6 +1257,7 @@ static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs&
   a.P = ctx->tr_P.as<double>();
   a.cache = nullptr;
   a.dz = nullptr;
+  a.pvalid = nullptr;
   a.draw = ctx->tr_draw.as<double>();
   a.raw = ctx->tr_raw.as<double>();
   a.B = (int)B;
@@ -1284,15 +1286,19 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
   tr::TrainArgs a;
   int rc = train_args(ctx, idx, B, a);
   if (rc) return rc;
+  const bool grouped = ctx->tr_H == tr::GH && !getenv("TS_TRAIN_WARP");
+  const int64_t K = (int64_t)ctx->tr_Tmax * B;
   TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
-  TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * B * ctx->tr_Tmax * L.G));
+  TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * K * (grouped ? tr::PROW : L.G)));
   a.cache = ctx->tr_cache.as<double>();
   a.dz = ctx->tr_dz.as<double>();
   a.target_scale = target_scale;
   a.n_total = (double)n_total;
-  const int64_t K = (int64_t)ctx->tr_Tmax * B;
   int ksplit;
-  if (ctx->tr_H == tr::GH && !getenv("TS_TRAIN_WARP")) {
+  if (grouped) {
+    TS_CUDA(ctx->tr_pvalid.reserve(K));
+    TS_CUDA(cudaMemsetAsync(ctx->tr_pvalid.p, 0, K, ctx->stream));
+    a.pvalid = ctx->tr_pvalid.as<uint8_t>();
     // grouped kernels (bit-identical forward/BPTT; weight gradients in the
     // same pair order within each of ksplit ranges)
     TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group, cudaFuncAttributeMaxDynamicSharedMemorySize,

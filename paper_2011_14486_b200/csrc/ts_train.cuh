@@ -66,7 +66,8 @@ struct TrainArgs {
   const int* batch;     // [B] dataset indices
   const double* P;      // params
   double* cache;        // [B][Tmax][8][H]
-  double* dz;           // [B][Tmax][4H]
+  double* dz;           // [B][Tmax][4H]  (grouped kernels: packed pair rows, below)
+  uint8_t* pvalid;      // grouped kernels: [Tmax * B] pair valid flags
   double* draw;         // [B]
   double* raw;          // [B]
   int B, Tmax, H;
@@ -259,7 +260,14 @@ __global__ void k_train_apply(double* __restrict__ P, const double* __restrict__
 // sequences), so each thread carries 8 (resp. 2) independent chains.  Every
 // output keeps the warp kernels' summation order and non-fused mul/add, so
 // the results are bit-identical to k_train_fb (tested).
+//
+// For the weight gradients the kernel also writes one packed row per valid
+// (sequence, timestep) pair at its position kk = (Tmax-1-t)*B + b of the
+// k_train_wgrad reduction order: [x_t (16) | h_{t-1} (32) | h_t (32) |
+// dz_t (128)], flag pvalid[kk] = 1, so k_train_wgrad_group streams
+// contiguous rows instead of chasing per-pair indices.
 constexpr int GS = 16;
+constexpr int PROW = 208;  // packed pair row (doubles)
 constexpr int GTHREADS = 256;
 constexpr int GH = 32, GG = 128, GK = 48;
 
@@ -308,7 +316,10 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       double v = 0.0;
       if (b < a.B) {
         const int i = a.batch[b];
-        if (t < a.D.Tlen[i]) v = a.D.x(i, t)[k];
+        if (t < a.D.Tlen[i]) {
+          v = a.D.x(i, t)[k];
+          a.dz[((int64_t)(a.Tmax - 1 - t) * a.B + b) * PROW + k] = v;
+        }
       }
       S.xh[s][k] = v;
     }
@@ -346,9 +357,12 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       cc[2 * GH + lane] = gg;
       cc[3 * GH + lane] = go;
       cc[4 * GH + lane] = c_prev;
-      cc[5 * GH + lane] = h_prev;
       cc[6 * GH + lane] = tc;
-      cc[7 * GH + lane] = h;
+      const int64_t kk = (int64_t)(a.Tmax - 1 - t) * a.B + g0 + s;
+      double* pr = a.dz + kk * PROW;
+      pr[16 + lane] = h_prev;
+      pr[48 + lane] = h;
+      if (lane == 0) a.pvalid[kk] = 1;
       hn[q] = h;
       const double prod = fmul(h, S.w[lane]);
       double acc = 0.0;
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       const double dzf = fmul(fmul(df, gf), fsub(1.0, gf));
       const double dzg = fmul(dg, fsub(1.0, fmul(gg, gg)));
       const double dzo = fmul(fmul(d_o, go), fsub(1.0, go));
-      double* dzt = a.dz + ((int64_t)b * a.Tmax + t) * GG;
+      double* dzt = a.dz + ((int64_t)(a.Tmax - 1 - t) * a.B + b) * PROW + 80;
       dzt[lane] = dzi;
       dzt[GH + lane] = dzf;
       dzt[2 * GH + lane] = dzg;
@@ -419,16 +433,17 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
 }
 
 // Weight gradients, H = 32: one CTA per k-split range of the (t descending,
-// b) pair sequence, all 6,305 parameters per CTA.  Chunks of WCH pairs are
-// staged in shared memory ([x | h_prev], dz, h, d_raw); thread (rg, cg) owns
-// the 3 x 8 block rows rg + 16i, columns cg + 16j of [dWx; dWh], threads
-// 0..127 also db, 128..159 dw, 160 db_out.  Each parameter is accumulated in
-// pair order with non-fused mul/add, as in k_train_wgrad.
+// b) pair sequence, all 6,305 parameters per CTA.  Chunks of WCH packed pair
+// rows are staged in shared memory (the next chunk is prefetched into
+// registers while the current one is consumed); thread (rg, cg) owns the
+// 3 x 8 block rows rg + 16i, columns cg + 16j of [dWx; dWh], threads 0..127
+// also db, 128..159 dw, 160 db_out.  Each parameter is accumulated in pair
+// order with non-fused mul/add, as in k_train_wgrad.
 constexpr int WCH = 16;
+constexpr int WV = WCH * PROW / 2;                      // 16-byte vectors per chunk
+constexpr int WPT = (WV + GTHREADS - 1) / GTHREADS;     // per thread
 struct WgradSmem {
-  double A[WCH][GK];
-  double D[WCH][GG];
-  double Hh[WCH][GH];
+  double R[WCH][PROW];
   double dr[WCH];
   double tdr[WCH];     // T * d_raw (db_out term, rows with t == 0)
   int valid[WCH];
@@ -450,53 +465,62 @@ __global__ void __launch_bounds__(GTHREADS) k_train_wgrad_group(TrainArgs a, int
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
   double extra = 0.0;
-  for (int64_t kb = k0; kb < k1; kb += WCH) {
+  // register prefetch of one chunk: rows [kb, kb + nk) are contiguous
+  uint4 pf[WPT];
+  int pf_valid = 0, pf_first = 0;
+  double pf_dr = 0.0, pf_tdr = 0.0;
+  auto fetch = [&](int64_t kb) {
     const int nk = (int)(k1 - kb < WCH ? k1 - kb : WCH);
-    __syncthreads();  // previous chunk consumed
+    const uint4* src = reinterpret_cast<const uint4*>(a.dz + kb * PROW);
+#pragma unroll
+    for (int v = 0; v < WPT; ++v) {
+      const int e = tid + v * GTHREADS;
+      if (e < nk * (PROW / 2)) pf[v] = __ldcs(src + e);  // invalid rows: unused bytes
+    }
     if (tid < nk) {
       const int64_t kk = kb + tid;
       const int t = a.Tmax - 1 - (int)(kk / a.B);
       const int b = (int)(kk % a.B);
-      const int T = a.D.Tlen[a.batch[b]];
-      S.valid[tid] = t < T;
-      S.first[tid] = t == 0;
-      S.dr[tid] = a.draw[b];
-      S.tdr[tid] = fmul((double)T, a.draw[b]);
+      pf_valid = a.pvalid[kk];
+      pf_first = t == 0;
+      pf_dr = a.draw[b];
+      pf_tdr = pf_first ? fmul((double)a.D.Tlen[a.batch[b]], pf_dr) : 0.0;
     }
-    __syncthreads();
-    // stage rows: 16 x, 32 h_prev, 32 h, 128 dz per pair
-    for (int e = tid; e < nk * 208; e += GTHREADS) {
-      const int rr = e / 208, f = e % 208;
-      if (!S.valid[rr]) continue;
-      const int64_t kk = kb + rr;
-      const int t = a.Tmax - 1 - (int)(kk / a.B);
-      const int b = (int)(kk % a.B);
-      const int64_t bt = (int64_t)b * a.Tmax + t;
-      if (f < 16) {
-        S.A[rr][f] = a.D.x(a.batch[b], t)[f];
-      } else if (f < 48) {
-        S.A[rr][f] = a.cache[(bt * CACHE_FIELDS + 5) * GH + (f - 16)];
-      } else if (f < 80) {
-        S.Hh[rr][f - 48] = a.cache[(bt * CACHE_FIELDS + 7) * GH + (f - 48)];
-      } else {
-        S.D[rr][f - 80] = a.dz[bt * GG + (f - 80)];
+  };
+  if (k0 < k1) fetch(k0);
+  for (int64_t kb = k0; kb < k1; kb += WCH) {
+    const int nk = (int)(k1 - kb < WCH ? k1 - kb : WCH);
+    __syncthreads();  // previous chunk consumed
+    {
+      uint4* dst = reinterpret_cast<uint4*>(&S.R[0][0]);
+#pragma unroll
+      for (int v = 0; v < WPT; ++v) {
+        const int e = tid + v * GTHREADS;
+        if (e < nk * (PROW / 2)) dst[e] = pf[v];
+      }
+      if (tid < nk) {
+        S.valid[tid] = pf_valid;
+        S.first[tid] = pf_first;
+        S.dr[tid] = pf_dr;
+        S.tdr[tid] = pf_tdr;
       }
     }
     __syncthreads();
+    if (kb + WCH < k1) fetch(kb + WCH);
     for (int rr = 0; rr < nk; ++rr) {
-      if (tid == 160 && S.first[rr]) extra = fadd(extra, S.tdr[rr]);
+      if (tid == GG + GH && S.first[rr]) extra = fadd(extra, S.tdr[rr]);
       if (!S.valid[rr]) continue;  // uniform
       double av[3], dv[8];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) av[i] = S.A[rr][rg + 16 * i];
+      for (int i = 0; i < 3; ++i) av[i] = S.R[rr][rg + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) dv[j] = S.D[rr][cg + 16 * j];
+      for (int j = 0; j < 8; ++j) dv[j] = S.R[rr][80 + cg + 16 * j];
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = fadd(acc[i][j], fmul(av[i], dv[j]));
-      if (tid < GG) extra = fadd(extra, S.D[rr][tid]);
-      else if (tid < GG + GH) extra = fadd(extra, fmul(S.Hh[rr][tid - GG], S.dr[rr]));
+      if (tid < GG) extra = fadd(extra, S.R[rr][80 + tid]);
+      else if (tid < GG + GH) extra = fadd(extra, fmul(S.R[rr][48 + tid - GG], S.dr[rr]));
     }
   }
   double* out = partial + (int64_t)blockIdx.x * L.n;
