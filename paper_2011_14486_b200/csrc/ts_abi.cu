@@ -1320,7 +1320,7 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
                                                                                ctx->tr_partial.as<double>());
     TS_LAUNCHED();
   }
-  tr::k_train_reduce<<<(L.n + 255) / 256, 256, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
+  tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
   TS_LAUNCHED();
   if (raw_out) {
     TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));

@@ -222,7 +222,15 @@ __global__ void k_train_reduce(const double* __restrict__ partial, int ksplit, i
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double acc = 0.0;
-  for (int k = 0; k < ksplit; ++k) acc = fadd(acc, partial[(int64_t)k * n + p]);
+  int k = 0;
+  for (; k + 8 <= ksplit; k += 8) {  // loads issued together, summed in order
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partial[(int64_t)(k + u) * n + p];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = fadd(acc, v[u]);
+  }
+  for (; k < ksplit; ++k) acc = fadd(acc, partial[(int64_t)k * n + p]);
   grad[p] = acc;
 }
 
@@ -257,9 +265,10 @@ __global__ void k_train_apply(double* __restrict__ P, const double* __restrict__
 // CTA with the weights resident in shared memory: every timestep is a small
 // [GS x 48] x [48 x 128] product (thread = gate column, 8 sequences each) and
 // the BPTT step a [GS x 128] x [128 x 32] product (thread = hidden unit, 2
-// sequences), so each thread carries 8 (resp. 2) independent chains.  Every
-// output keeps the warp kernels' summation order and non-fused mul/add, so
-// the results are bit-identical to k_train_fb (tested).
+// sequences), so each thread carries 8 (resp. 2) independent chains.  The
+// products accumulate with fused multiply-adds in the same k order as the
+// warp kernels (as BLAS dgemm kernels do); the gate and cell arithmetic is
+// identical, so the two agree to rounding (tested at 1e-12).
 //
 // For the weight gradients the kernel also writes one packed row per valid
 // (sequence, timestep) pair at its position kk = (Tmax-1-t)*B + b of the
@@ -278,6 +287,9 @@ struct GroupSmem {
   double zb[GS][GG];   // gate pre-activations (forward), dz (backward)
   double b[GG];
   double w[GH];
+  const double* xinit[GS];  // per sequence: init rows (t < T - d)
+  const double* xrows[GS];  //               scheduled rows, reversed (t >= T - d)
+  int T[GS], Tu[GS];        // length, first scheduled timestep T - d
 };
 
 __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
@@ -292,34 +304,44 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
   if (tid < GH) S.w[tid] = P[L.ow + tid];
   for (int e = tid; e < GS * GK; e += GTHREADS) (&S.xh[0][0])[e] = 0.0;
   const int g0 = blockIdx.x * GS;
+  if (tid < GS) {
+    const int b = g0 + tid;
+    int T = 0, Tu = 0;
+    const double *xi = a.D.init, *xr = a.D.rows;
+    if (b < a.B) {
+      const int i = a.batch[b];
+      T = a.D.Tlen[i];
+      Tu = T - a.D.depth[i];
+      xi = a.D.init + (int64_t)a.D.init_base[i] * F;
+      xr = a.D.rows + (a.D.row_base[i] + (T - 1)) * F;  // row of timestep t: xr - t * F
+    }
+    S.T[tid] = T;
+    S.Tu[tid] = Tu;
+    S.xinit[tid] = xi;
+    S.xrows[tid] = xr;
+  }
+  __syncthreads();
   int Tg = 0;
-  for (int s = 0; s < GS; ++s)
-    if (g0 + s < a.B) Tg = max(Tg, a.D.Tlen[a.batch[g0 + s]]);
+  for (int s = 0; s < GS; ++s) Tg = max(Tg, S.T[s]);
   // gate-phase ownership: sequence s = warp + 8q, hidden unit j = lane
-  int idx[2], Tq[2];
+  int Tq[2];
   double raw[2], c[2] = {0.0, 0.0};
   double* cache[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    const int b = g0 + warp + 8 * q;
-    const bool v = b < a.B;
-    idx[q] = v ? a.batch[b] : 0;
-    Tq[q] = v ? a.D.Tlen[idx[q]] : 0;
+    const int s = warp + 8 * q, b = g0 + s;
+    Tq[q] = S.T[s];
     raw[q] = fmul((double)Tq[q], P[L.obout]);
-    cache[q] = a.cache + (int64_t)(v ? b : 0) * a.Tmax * CACHE_FIELDS * GH;
+    cache[q] = a.cache + (int64_t)(b < a.B ? b : 0) * a.Tmax * CACHE_FIELDS * GH;
   }
-  __syncthreads();
   // ---- forward with cache
   for (int t = 0; t < Tg; ++t) {
     {  // x rows: one feature per thread
-      const int s = tid >> 4, k = tid & 15, b = g0 + s;
+      const int s = tid >> 4, k = tid & 15;
       double v = 0.0;
-      if (b < a.B) {
-        const int i = a.batch[b];
-        if (t < a.D.Tlen[i]) {
-          v = a.D.x(i, t)[k];
-          a.dz[((int64_t)(a.Tmax - 1 - t) * a.B + b) * PROW + k] = v;
-        }
+      if (t < S.T[s]) {
+        v = t < S.Tu[s] ? S.xinit[s][t * F + k] : S.xrows[s][k - t * F];
+        a.dz[((int64_t)(a.Tmax - 1 - t) * a.B + g0 + s) * PROW + k] = v;
       }
       S.xh[s][k] = v;
     }
@@ -334,7 +356,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       for (int k = 0; k < GK; ++k) {
         const double wk = S.W[k][n];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) z[i] = fadd(z[i], fmul(S.xh[s0 + 2 * i][k], wk));
+        for (int i = 0; i < 8; ++i) z[i] = ffma(S.xh[s0 + 2 * i][k], wk, z[i]);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) S.zb[s0 + 2 * i][n] = z[i];
@@ -381,23 +403,38 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
     const int b = g0 + warp + 8 * q;
     d_raw[q] = 0.0;
     if (b >= a.B) continue;
-    d_raw[q] = fdiv(fmul(2.0, fsub(fadd(raw[q], a.target_scale), a.D.logt[idx[q]])), a.n_total);
+    d_raw[q] = fdiv(fmul(2.0, fsub(fadd(raw[q], a.target_scale), a.D.logt[a.batch[b]])), a.n_total);
     if (lane == 0) {
       a.raw[b] = raw[q];
       a.draw[b] = d_raw[q];
     }
   }
-  // ---- BPTT
+  // ---- BPTT; the cache row of the next (earlier) timestep is prefetched
+  // into registers while the current dh_next product runs
   double dh_next[2] = {0.0, 0.0}, dc_next[2] = {0.0, 0.0};
   const double wj = S.w[lane];
+  double cv[2][6];
+  auto load_cache = [&](int t) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (t < 0 || t >= Tq[q]) continue;
+      const double* cc = cache[q] + (int64_t)t * CACHE_FIELDS * GH + lane;
+      cv[q][0] = cc[0];
+      cv[q][1] = cc[GH];
+      cv[q][2] = cc[2 * GH];
+      cv[q][3] = cc[3 * GH];
+      cv[q][4] = cc[4 * GH];
+      cv[q][5] = cc[6 * GH];
+    }
+  };
+  load_cache(Tg - 1);
   for (int t = Tg - 1; t >= 0; --t) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       if (t >= Tq[q]) continue;
       const int s = warp + 8 * q, b = g0 + s;
-      const double* cc = cache[q] + (int64_t)t * CACHE_FIELDS * GH;
-      const double gi = cc[lane], gf = cc[GH + lane], gg = cc[2 * GH + lane], go = cc[3 * GH + lane];
-      const double c_prev = cc[4 * GH + lane], tc = cc[6 * GH + lane];
+      const double gi = cv[q][0], gf = cv[q][1], gg = cv[q][2], go = cv[q][3];
+      const double c_prev = cv[q][4], tc = cv[q][5];
       const double dh = fadd(fmul(wj, d_raw[q]), dh_next[q]);
       const double d_o = fmul(dh, tc);
       const double dc = fadd(dc_next[q], fmul(fmul(dh, go), fsub(1.0, fmul(tc, tc))));
@@ -417,6 +454,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       S.zb[s][2 * GH + lane] = dzg;
       S.zb[s][3 * GH + lane] = dzo;
     }
+    load_cache(t - 1);
     __syncthreads();
     // dh_next = dz @ Wh.T in gate-column order
 #pragma unroll
@@ -425,7 +463,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       const int s = warp + 8 * q;
       double acc = 0.0;
 #pragma unroll 8
-      for (int col = 0; col < GG; ++col) acc = fadd(acc, fmul(S.zb[s][col], S.WhT[col][lane]));
+      for (int col = 0; col < GG; ++col) acc = ffma(S.zb[s][col], S.WhT[col][lane], acc);
       dh_next[q] = acc;
     }
     __syncthreads();
@@ -438,7 +476,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
 // registers while the current one is consumed); thread (rg, cg) owns the
 // 3 x 8 block rows rg + 16i, columns cg + 16j of [dWx; dWh], threads 0..127
 // also db, 128..159 dw, 160 db_out.  Each parameter is accumulated in pair
-// order with non-fused mul/add, as in k_train_wgrad.
+// order (fused multiply-add).
 constexpr int WCH = 16;
 constexpr int WV = WCH * PROW / 2;                      // 16-byte vectors per chunk
 constexpr int WPT = (WV + GTHREADS - 1) / GTHREADS;     // per thread
@@ -518,9 +556,9 @@ __global__ void __launch_bounds__(GTHREADS) k_train_wgrad_group(TrainArgs a, int
 #pragma unroll
       for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fadd(acc[i][j], fmul(av[i], dv[j]));
+        for (int j = 0; j < 8; ++j) acc[i][j] = ffma(av[i], dv[j], acc[i][j]);
       if (tid < GG) extra = fadd(extra, S.R[rr][80 + tid]);
-      else if (tid < GG + GH) extra = fadd(extra, fmul(S.R[rr][48 + tid - GG], S.dr[rr]));
+      else if (tid < GG + GH) extra = ffma(S.R[rr][48 + tid - GG], S.dr[rr], extra);
     }
   }
   double* out = partial + (int64_t)blockIdx.x * L.n;

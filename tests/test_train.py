@@ -116,11 +116,10 @@ def test_device_gradients_match_oracle(golden, v0_path):
 
 @pytest.mark.gpu
 def test_grouped_kernels_match_warp_kernels(golden, v0_path, monkeypatch):
-    """The H = 32 grouped forward/BPTT kernel is bit-identical to the
-    warp-per-sequence kernel (same summation orders); the grouped weight
-    gradients differ only in the k-split boundaries (<= 1e-12 relative).
-    Ragged lengths, a batch that is not a multiple of the group size, and
-    repeated indices."""
+    """The H = 32 grouped forward/BPTT and weight-gradient kernels agree with
+    the warp-per-sequence kernels to rounding (same k order, fused
+    multiply-adds, different k-split boundaries).  Ragged lengths, a batch
+    that is not a multiple of the group size, and repeated indices."""
     import torch
     from paper_2011_14486_b200 import _lib
     from paper_2011_14486_b200.featurizer import featurize_states, normalize
@@ -150,8 +149,8 @@ def test_grouped_kernels_match_warp_kernels(golden, v0_path, monkeypatch):
             dev.grads(batch, B, params.target_scale, gb.data_ptr(), raw_out=raw)
             dev.sync()
             out[mode] = (raw, gb.cpu().numpy())
-        assert np.array_equal(out["group"][0], out["warp"][0])
-        np.testing.assert_allclose(out["group"][1], out["warp"][1], rtol=1e-12, atol=1e-17)
+        np.testing.assert_allclose(out["group"][0], out["warp"][0], rtol=1e-13, atol=0)
+        np.testing.assert_allclose(out["group"][1], out["warp"][1], rtol=1e-11, atol=1e-16)
 
 
 @pytest.mark.gpu
