@@ -352,11 +352,14 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       const double bn = S.b[n];
 #pragma unroll
       for (int i = 0; i < 8; ++i) z[i] = bn;
-#pragma unroll 4
-      for (int k = 0; k < GK; ++k) {
-        const double wk = S.W[k][n];
+#pragma unroll 2
+      for (int k = 0; k < GK; k += 2) {  // k order kept; x pairs as 16-byte loads
+        const double w0 = S.W[k][n], w1 = S.W[k + 1][n];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) z[i] = ffma(S.xh[s0 + 2 * i][k], wk, z[i]);
+        for (int i = 0; i < 8; ++i) {
+          const double2 xv = *reinterpret_cast<const double2*>(&S.xh[s0 + 2 * i][k]);
+          z[i] = ffma(xv.y, w1, ffma(xv.x, w0, z[i]));
+        }
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) S.zb[s0 + 2 * i][n] = z[i];
@@ -456,15 +459,20 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
     }
     load_cache(t - 1);
     __syncthreads();
-    // dh_next = dz @ Wh.T in gate-column order
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      if (t >= Tq[q]) continue;
-      const int s = warp + 8 * q;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int col = 0; col < GG; ++col) acc = ffma(S.zb[s][col], S.WhT[col][lane], acc);
-      dh_next[q] = acc;
+    // dh_next = dz @ Wh.T in gate-column order; both sequences share the
+    // Wh loads, dz pairs as 16-byte broadcasts
+    {
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 4
+      for (int col = 0; col < GG; col += 2) {
+        const double w0 = S.WhT[col][lane], w1 = S.WhT[col + 1][lane];
+        const double2 z0 = *reinterpret_cast<const double2*>(&S.zb[warp][col]);
+        const double2 z1 = *reinterpret_cast<const double2*>(&S.zb[warp + 8][col]);
+        acc0 = ffma(z0.y, w1, ffma(z0.x, w0, acc0));
+        acc1 = ffma(z1.y, w1, ffma(z1.x, w0, acc1));
+      }
+      if (t < Tq[0]) dh_next[0] = acc0;
+      if (t < Tq[1]) dh_next[1] = acc1;
     }
     __syncthreads();
   }
