@@ -426,7 +426,7 @@ def main():
     # kernel at 262,144 states, scaled to this launch
     traffic_per_state = {"featurize": (100.080128e6 + 368.331776e6) / 262144,
                          "lstm_fast": (309.275648e6 + 4.245760e6) / 262144}
-    row_bytes = 64 if mode == _lib.MODE_FAST else ROW_BYTES
+    row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
         bytes_per_launch = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
         achieved = bytes_per_launch / (avg[dom] / 1e3) / 1e9

@@ -635,7 +635,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       tc::k_depth_scatter<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, cursor, perm);
       TS_LAUNCHED();
     }
-    TS_CUDA(ctx->rows.reserve(sizeof(float) * F * (n_records > 0 ? n_records : 1)));
+    TS_CUDA(ctx->rows.reserve(sizeof(float) * 8 * (n_records > 0 ? n_records : 1)));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(

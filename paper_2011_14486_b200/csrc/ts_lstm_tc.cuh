@@ -226,7 +226,7 @@ __device__ __forceinline__ void put_bias_ones(uint8_t* A, int r) {
 struct TcArgs {
   const uint8_t* wpack;     // B' image (TILE_BYTES) + readout w[32] f32
   const float* init32;      // [T][16] normalized unscheduled rows (fp32)
-  const float* rows32;      // [n_records][16] normalized scheduled rows (fp32)
+  const float* rows32;      // [n_records][8] normalized acquired features of scheduled rows (fp32)
   const int64_t* offsets;   // [n+1]
   const int* perm;          // [n] sorted position -> state
   const int64_t* rowoff;    // [T+1] decision-major row offsets (k_depth_scan)
@@ -240,16 +240,17 @@ struct TcArgs {
   double b_out;
 };
 
-__device__ __forceinline__ void load_x(const float* src, float* x) {
-  const float4* s4 = reinterpret_cast<const float4*>(src);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float4 v = __ldg(s4 + q);
-    x[4 * q] = v.x;
-    x[4 * q + 1] = v.y;
-    x[4 * q + 2] = v.z;
-    x[4 * q + 3] = v.w;
-  }
+// x at timestep t: intrinsic half from the stage's init row (the same for
+// every row of the tile), acquired half from the init row (unscheduled) or
+// the state's scheduled row
+__device__ __forceinline__ void load_x(const float* init_row, const float* acq, float* x) {
+  const float4* i4 = reinterpret_cast<const float4*>(init_row);
+  const float4* a4 = reinterpret_cast<const float4*>(acq);
+  const float4 v0 = __ldg(i4), v1 = __ldg(i4 + 1), v2 = __ldg(a4), v3 = __ldg(a4 + 1);
+  x[0] = v0.x, x[1] = v0.y, x[2] = v0.z, x[3] = v0.w;
+  x[4] = v1.x, x[5] = v1.y, x[6] = v1.z, x[7] = v1.w;
+  x[8] = v2.x, x[9] = v2.y, x[10] = v2.z, x[11] = v2.w;
+  x[12] = v3.x, x[13] = v3.y, x[14] = v3.z, x[15] = v3.w;
 }
 
 __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
@@ -331,7 +332,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       for (int g8 = 0; g8 < 4; ++g8) put_h8(A, r, g8, h0 + 8 * g8);
     }
     float x[16];
-    load_x((t0 < T - d) ? a.init32 + t0 * 16 : a.rows32 + (a.rowoff[T - 1 - t0] + sp) * 16, x);
+    load_x(a.init32 + t0 * 16, (t0 < T - d) ? a.init32 + t0 * 16 + 8 : a.rows32 + (a.rowoff[T - 1 - t0] + sp) * 8,
+           x);
     for (int t = t0; t < T; ++t) {
       put_x(A, r, x);
       fence_async_smem();
@@ -347,7 +349,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       }
       // prefetch the next row while the tensor core works
       if (t + 1 < T)
-        load_x((t + 1 < T - d) ? a.init32 + (t + 1) * 16 : a.rows32 + (a.rowoff[T - 2 - t] + sp) * 16, x);
+        load_x(a.init32 + (t + 1) * 16,
+               (t + 1 < T - d) ? a.init32 + (t + 1) * 16 + 8 : a.rows32 + (a.rowoff[T - 2 - t] + sp) * 8, x);
       mbar_wait(bar, phase);
       phase ^= 1u;
       fence_after();
