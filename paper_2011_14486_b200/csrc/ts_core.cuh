@@ -463,6 +463,13 @@ struct Nest {
   uint8_t id[TS_MAX_LOOPS];   // loop ids (ts_decision.order encoding)
   int32_t n_loops;
   int32_t depth;
+  // accessors shared with views of a nest stored elsewhere (the device's
+  // shared-memory slots), so the nest math reads a consumer nest in place
+  TS_HD uint64_t inv_w(int k) const { return inv.w[k]; }
+  TS_HD uint32_t ext_at(int j) const { return ext[j]; }
+  TS_HD uint8_t id_at(int j) const { return id[j]; }
+  TS_HD int loops() const { return n_loops; }
+  TS_HD int dep() const { return depth; }
 };
 
 TS_HD int loop_dim(uint8_t id, int n_pure) { return id < 8 ? (id >> 1) : n_pure + (id - 8); }
@@ -488,27 +495,28 @@ TS_HD bool anchor_ok(const Nest& c, int lvl) {
 // Per-invocation pure extents, invocations and depth of stage `s` anchored
 // at level `lvl` of its sole consumer's nest (schedule_space.py:190-225).
 // Returns TS_OK / TS_ERR_OVERFLOW.
-TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& cn, int lvl,
+template <class CN>
+TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn, int lvl,
                            int64_t* pe, u256& inv, int& depth) {
   // invocations = consumer invocations * prod(outer loop extents up to lvl);
   // a 128-bit path covers all but the deepest chains (branch-uniform within
   // a warp far more often than a 64/256 split), 256 bits the rest
   bool ok = true;
   {
-    unsigned __int128 p = ((unsigned __int128)cn.inv.w[1] << 64) | cn.inv.w[0];
-    bool fit = cn.inv.w[2] == 0 && cn.inv.w[3] == 0;
+    unsigned __int128 p = ((unsigned __int128)cn.inv_w(1) << 64) | cn.inv_w(0);
+    bool fit = cn.inv_w(2) == 0 && cn.inv_w(3) == 0;
 #pragma unroll
     for (int j = 0; j < TS_MAX_LOOPS; ++j)
-      if (j <= lvl && j < cn.n_loops) p = mul128_64(p, cn.ext[j], fit);
+      if (j <= lvl && j < cn.loops()) p = mul128_64(p, cn.ext_at(j), fit);
     if (fit) {
       inv.w[0] = (uint64_t)p;
       inv.w[1] = (uint64_t)(p >> 64);
       inv.w[2] = inv.w[3] = 0;
     } else {
-      inv = cn.inv;
+      for (int k = 0; k < 4; ++k) inv.w[k] = cn.inv_w(k);
 #pragma unroll
       for (int j = 0; j < TS_MAX_LOOPS; ++j)
-        if (j <= lvl && j < cn.n_loops) ok = u256_mul_u64(inv, cn.ext[j]) && ok;
+        if (j <= lvl && j < cn.loops()) ok = u256_mul_u64(inv, cn.ext_at(j)) && ok;
     }
   }
   // per-invocation consumer region: for each consumer dim read by an edge,
@@ -521,8 +529,8 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& 
     for (int k = 0; k < TS_MAX_PURE; ++k) rv[e][k] = 1u;
 #pragma unroll
   for (int j = 0; j < TS_MAX_LOOPS; ++j) {
-    const uint32_t m = (j > lvl && j < cn.n_loops) ? cn.ext[j] : 1u;
-    const int dim = loop_dim(cn.id[j], cs.n_pure);
+    const uint32_t m = (j > lvl && j < cn.loops()) ? cn.ext_at(j) : 1u;
+    const int dim = loop_dim(cn.id_at(j), cs.n_pure);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
@@ -541,16 +549,17 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const Nest& 
     }
     pe[k] = best;
   }
-  depth = cn.depth + lvl + 1;
+  depth = cn.dep() + lvl + 1;
   return ok ? TS_OK : TS_ERR_OVERFLOW;
 }
 
 // _nest_entry/_build_loops (schedule_space.py:228-274).  `cn` may be null
 // for Root decisions; pe receives the per-invocation pure extents.
-TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const Nest* cn, const ts_decision& d,
+template <class CN = Nest>
+TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, const ts_decision& d,
                      Nest& out, int64_t* pe) {
   if (d.anchor >= 0) {
-    if (!cn || !cs || d.anchor >= cn->n_loops) return TS_ERR_ILLEGAL;
+    if (!cn || !cs || d.anchor >= cn->loops()) return TS_ERR_ILLEGAL;
     const int rc = anchored_extents(s, *cs, *cn, d.anchor, pe, out.inv, out.depth);
     if (rc) return rc;
   } else {
