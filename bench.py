@@ -389,15 +389,26 @@ def main():
     h_out = torch.empty(M, dtype=torch.float64, pin_memory=True)
     # the 8-byte wire format (ts_score_states_packed): what predict_states
     # sends for large batches
-    packed = _lib.pack_records(np.frombuffer(h_recs.numpy().tobytes(), dtype=_lib.DECISION_DTYPE))
-    assert packed is not None
-    h_packed = torch.from_numpy(packed.view(np.int64)).pin_memory()
+    # the wire format predict_states sends for large batches: 16-bit action
+    # codes (ts_score_states_coded) when every decision is in
+    # candidate_actions' space (always, for these walks), else 8-byte packed
+    from paper_2011_14486_b200.schedule_space import action_codes
+    np_recs = np.frombuffer(h_recs.numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
+    codes = action_codes(inf, np_recs, h_offs.numpy())
     h_depth = torch.from_numpy(np.diff(h_offs.numpy()).astype(np.uint8)).pin_memory()
-    e2e_h2d = int(packed.nbytes + M)
+    if codes is not None:
+        h_wire = torch.from_numpy(codes.view(np.int16)).pin_memory()
+        wire_name = "16-bit action codes + u8 depths (ts_score_states_coded)"
+        wire_fn = ctx.lib.ts_score_states_coded
+    else:
+        packed = _lib.pack_records(np_recs)
+        h_wire = torch.from_numpy(packed.view(np.int64)).pin_memory()
+        wire_name = "8-byte packed decisions + u8 depths (ts_score_states_packed)"
+        wire_fn = ctx.lib.ts_score_states_packed
+    e2e_h2d = int(h_wire.numel() * h_wire.element_size() + M)
 
     def e2e_step():
-        ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, h_packed.data_ptr(), h_depth.data_ptr(), M,
-                                                 mode, h_out.data_ptr()))
+        ctx.check(wire_fn(ctx.h, pid, h_wire.data_ptr(), h_depth.data_ptr(), M, mode, h_out.data_ptr()))
 
     for _ in range(2):
         e2e_step()
@@ -490,8 +501,7 @@ def main():
                        "mode": args.mode, "l2": "inputs larger than L2 (records "
                        f"{n_records * 16 / 1e6:.0f} MB/GPU)", "parallelism": f"shard{world}"},
             "e2e": {"value": e2e_value, "unit": "states/s",
-                    "h2d_bytes_per_step": e2e_h2d, "wire_format": "8-byte packed decisions + u8 depths "
-                                                                  "(ts_score_states_packed)",
+                    "h2d_bytes_per_step": e2e_h2d, "wire_format": wire_name,
                     "d2h_bytes_per_step": int(8 * M)},
             "gpu_launches": int(launches),
             "roofline": roof,

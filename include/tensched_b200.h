@@ -122,6 +122,31 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records,
 int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed, const uint8_t* depths,
                            int64_t n_states, int mode, double* out_v);
 
+/* Action-code wire format: one 16-bit code per decision for decisions in
+ * candidate_actions' space (schedule_space.py:379-452; SPLIT_FACTORS (8, 32),
+ * VEC_WIDTHS (1, 8), compute_at levels 0..2, orders from _order_options
+ * :361-376), decoded against the decision's stage on the device inside the
+ * featurizer:
+ *   bits 0-1  compute_at level + 1 (0 = root)
+ *   bits 2-3  split of splittable dim 0 (dims[-2:][0]): 0 none, 1 -> 8, 2 -> 32
+ *   bits 4-5  split of splittable dim 1 (dims[-2:][1], if the stage has two)
+ *   bit  6    order placement: reduction loops outermost (else innermost)
+ *   bit  7    order swap: last two loops exchanged
+ *   bit  8    vectorize 8 (else 1)
+ *   bit  9    parallel
+ *   bit  10   store_at = compute_at site
+ *   bits 11-15 zero
+ * plus one u8 depth per state: 1/8 of the PCIe bytes of ts_score_states.
+ * Callers fall back to the packed or record formats for other decisions. */
+#define TS_CODE_SPACE 2048  /* 11-bit action codes */
+int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
+                          int64_t n_states, int mode, double* out_v);
+
+/* Decodes action codes to records on the host (state i's decision j belongs
+ * to schedule position j); for tests and tools.  Host-only contexts work. */
+int ts_decode_codes(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
+                    int64_t n_states, ts_decision* out_records);
+
 /* Same with device-resident inputs/outputs (pointers into the context's
  * device), stream-ordered on the context stream. */
 int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,

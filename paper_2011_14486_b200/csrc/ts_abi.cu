@@ -81,6 +81,7 @@ struct PipelineSlot {
   DevBuf init_norm;  // [T][16]
   DevBuf pre_exact;  // [(T+1)][72]
   DevBuf pre_fast;   // fast-path prefix
+  DevBuf code_table; // [T][TS_CODE_SPACE + 1] decoded action codes (built on first coded call)
   uint64_t rows_version = 0;  // params version the init rows / prefix belong to
   uint64_t fast_version = 0;
 };
@@ -121,6 +122,7 @@ struct ts_ctx {
   int64_t tr_N = 0;
   DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm, tr_partial,
       tr_pvalid;
+  DevBuf tile_ctr;  // k_lstm_tc's dynamic tile counter
   tr::Data tr_data{};
 };
 
@@ -588,9 +590,10 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   return TS_OK;
 }
 
+// d_codes (optional): 16-bit action codes instead of records, same offsets
 static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_records,
                         const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
-                        double* d_out) {
+                        double* d_out, const uint16_t* d_codes = nullptr) {
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
   const int T = P->h->n_stages;
@@ -600,7 +603,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
-          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>(),
+          nullptr, nullptr, d_codes);
       TS_LAUNCHED();
     }
     {
@@ -641,7 +645,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>(),
-          perm, rowoff);
+          perm, rowoff, d_codes);
       TS_LAUNCHED();
     }
     tc::TcArgs ta;
@@ -659,6 +663,9 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     ta.record_prefix = 0;
     ta.target_scale = ctx->target_scale;
     ta.b_out = ctx->b_out;
+    TS_CUDA(ctx->tile_ctr.reserve(sizeof(int)));
+    TS_CUDA(cudaMemsetAsync(ctx->tile_ctr.p, 0, sizeof(int), ctx->stream));
+    ta.tile_counter = ctx->tile_ctr.as<int>();
     {
       KTimer kt(ctx, TS_K_LSTM_FAST);
       const int grid = std::min((ta.n_tiles + tc::NWG - 1) / tc::NWG, ctx->sm_count);
@@ -673,6 +680,26 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
 // Host-path chunking: chunks overlap H2D with scoring; measured on B200
 // (1M VGG-16 states): 4 chunks beat 1 (no overlap) and 8-16 (per-chunk tile
 // tails), so ~n/4 capped at 2^18.
+// Sum of n bytes, eight at a time (SWAR, 16-bit lanes flushed every 128
+// words): the host-side record count of a depth vector.
+static uint64_t sum_bytes(const uint8_t* p, int64_t n) {
+  const uint64_t M = 0x00FF00FF00FF00FFull;
+  uint64_t total = 0;
+  int64_t i = 0;
+  while (i + 8 <= n) {
+    uint64_t lanes = 0;
+    for (int w = 0; w < 128 && i + 8 <= n; ++w, i += 8) {
+      uint64_t x;
+      memcpy(&x, p + i, 8);
+      lanes += (x & M) + ((x >> 8) & M);
+    }
+    lanes = (lanes & 0x0000FFFF0000FFFFull) + ((lanes >> 16) & 0x0000FFFF0000FFFFull);
+    total += (lanes & 0xFFFFFFFFull) + (lanes >> 32);
+  }
+  for (; i < n; ++i) total += p[i];
+  return total;
+}
+
 static int64_t e2e_chunk(int64_t n) {
   int64_t c = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 18, (n + 3) / 4));
   if (const char* e = getenv("TS_E2E_CHUNK")) c = std::max<int64_t>(1024, atoll(e));
@@ -780,9 +807,7 @@ int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed,
     for (int64_t k = 0; k < n_chunks; ++k) {
       rec_at[k] = acc;
       const int64_t s1 = std::min(n_states, (k + 1) * chunk);
-      uint64_t part = 0;
-      for (int64_t i = k * chunk; i < s1; ++i) part += depths[i];
-      acc += (int64_t)part;
+      acc += (int64_t)sum_bytes(depths + k * chunk, s1 - k * chunk);
     }
     rec_at[n_chunks] = acc;
   }
@@ -837,6 +862,103 @@ int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed,
   TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   for (auto e : ev) ctx->event_pool.push_back(e);
   return check_device_status(ctx);
+}
+
+int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
+                          int64_t n_states, int mode, double* out_v) {
+  if (!ctx || !depths || !out_v || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  if (mode == TS_MODE_FAST) {
+    rc = ensure_fast_prefix(ctx, P);
+    if (rc) return rc;
+  }
+  // codes are 1/8 of the record bytes, so two chunks hide the transfer
+  int64_t chunk = std::max<int64_t>(1 << 16, (n_states + 1) / 2);
+  if (const char* e = getenv("TS_CODED_CHUNK")) chunk = std::max<int64_t>(1024, atoll(e));
+  if (chunk > n_states) chunk = n_states;
+  const int64_t n_chunks = (n_states + chunk - 1) / chunk;
+  std::vector<int64_t> rec_at(n_chunks + 1);
+  {
+    int64_t acc = 0;
+    for (int64_t k = 0; k < n_chunks; ++k) {
+      rec_at[k] = acc;
+      const int64_t s1 = std::min(n_states, (k + 1) * chunk);
+      acc += (int64_t)sum_bytes(depths + k * chunk, s1 - k * chunk);
+    }
+    rec_at[n_chunks] = acc;
+  }
+  const int64_t n_rec = rec_at[n_chunks];
+  if (n_rec > 0 && !codes) return TS_ERR_ARG;
+  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
+  TS_CUDA(ctx->out.reserve(sizeof(double) * n_states));
+  TS_CUDA(ctx->tmp2.reserve(sizeof(uint16_t) * (n_rec > 0 ? n_rec : 1) + n_states + 64));
+  uint16_t* d_codes = ctx->tmp2.as<uint16_t>();
+  uint8_t* d_depth = reinterpret_cast<uint8_t*>(ctx->tmp2.as<uint8_t>() + ((sizeof(uint16_t) * n_rec + 15) & ~15ull));
+  int64_t* d_off = ctx->offsets.as<int64_t>();
+  TS_CUDA(cudaMemcpyAsync(d_depth, depths, n_states, cudaMemcpyHostToDevice, ctx->copy_stream));
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t dep = take_event(ctx);
+  TS_CUDA(cudaEventRecord(dep, ctx->copy_stream));
+  ev.push_back(dep);
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int64_t r0 = rec_at[k], r1 = rec_at[k + 1];
+    if (r1 > r0)
+      TS_CUDA(cudaMemcpyAsync(d_codes + r0, codes + r0, sizeof(uint16_t) * (r1 - r0), cudaMemcpyHostToDevice,
+                              ctx->copy_stream));
+    cudaEvent_t in = take_event(ctx);
+    ev.push_back(in);
+    TS_CUDA(cudaEventRecord(in, ctx->copy_stream));
+  }
+  if (!P->code_table.p) {  // every code of every stage, decoded once per pipeline
+    const int T = P->h->n_stages;
+    TS_CUDA(P->code_table.reserve(sizeof(ts_decision) * (size_t)T * (TS_CODE_SPACE + 1)));
+    k_code_table<<<(unsigned)((T * (TS_CODE_SPACE + 1) + 255) / 256), 256, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), T, P->code_table.as<ts_decision>());
+    TS_LAUNCHED();
+  }
+  TS_CUDA(cudaStreamWaitEvent(ctx->stream, dep, 0));
+  k_depths_to_counts<<<(unsigned)((n_states + 255) / 256), 256, 0, ctx->stream>>>(d_depth, n_states, d_off);
+  TS_LAUNCHED();
+  {
+    size_t temp = 0;
+    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + 1, d_off + 1, n_states, ctx->stream));
+    TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
+    TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, d_off + 1, d_off + 1, n_states, ctx->stream));
+    ++ctx->launches;
+  }
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int64_t s0 = k * chunk, s1 = std::min(n_states, s0 + chunk);
+    TS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k + 1], 0));
+    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, n_rec, mode,
+                      ctx->out.as<double>() + s0, d_codes);
+    if (rc) return rc;
+    TS_CUDA(cudaMemcpyAsync(out_v + s0, ctx->out.as<double>() + s0, sizeof(double) * (s1 - s0),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  for (auto e : ev) ctx->event_pool.push_back(e);
+  return check_device_status(ctx);
+}
+
+int ts_decode_codes(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
+                    int64_t n_states, ts_decision* out_records) {
+  if (!ctx || !depths || n_states < 0) return TS_ERR_ARG;
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  int64_t r = 0;
+  for (int64_t i = 0; i < n_states; ++i) {
+    if (depths[i] > T) return fail(ctx, TS_ERR_ARG, "depth exceeds the pipeline's stages");
+    for (int j = 0; j < depths[i]; ++j, ++r) out_records[r] = decode_action(D.st[T - 1 - j], codes[r]);
+  }
+  return TS_OK;
 }
 
 int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,

@@ -598,6 +598,65 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, cons
   return bad ? TS_ERR_ILLEGAL : TS_OK;
 }
 
+// 16-bit action code -> decision record for stage `s` (layout in
+// include/tensched_b200.h, ts_score_states_coded): the candidate_actions
+// space - splits of the innermost two pure dims by SPLIT_FACTORS, orders
+// from _order_options (schedule_space.py:361-376: pure then reduction loops
+// or the reverse, optionally with the last two exchanged), VEC_WIDTHS.
+TS_HD ts_decision decode_action(const StageDesc& s, uint32_t code) {
+  ts_decision d;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d.split[k] = 0;
+  const int np = s.n_pure, nr = s.n_red;
+  const int first = np >= 2 ? np - 2 : 0;  // splittable = dims[-2:]
+  const uint32_t sc0 = (code >> 2) & 3u, sc1 = (code >> 4) & 3u;
+  const uint8_t f0 = sc0 == 1 ? 8 : sc0 == 2 ? 32 : 0, f1 = sc1 == 1 ? 8 : sc1 == 2 ? 32 : 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < np) d.split[k] = k == first ? f0 : (k == first + 1 ? f1 : 0);
+  // pure loop ids (k -> 2k, split: 2k, 2k+1) and reduction ids (8 + r) in
+  // placement order, packed a byte per position (registers, not an array)
+  uint64_t seq = 0;
+  int n = 0;
+  auto push = [&](uint32_t id) {
+    if (n < TS_MAX_LOOPS) seq |= (uint64_t)id << (8 * n);
+    ++n;
+  };
+  const bool outer = (code >> 6) & 1u;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    if ((pass == 0) == outer) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (r < nr) push(8 + r);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < np) {
+          push(2 * k);
+          if (d.split[k]) push(2 * k + 1);
+        }
+    }
+  }
+  if (((code >> 7) & 1u) && n >= 2 && n <= TS_MAX_LOOPS) {
+    const int sa = 8 * (n - 2), sb = 8 * (n - 1);
+    const uint64_t a = (seq >> sa) & 0xFFu, b = (seq >> sb) & 0xFFu;
+    seq = (seq & ~(0xFFFFull << sa)) | (b << sa) | (a << sb);
+  }
+  if (n < TS_MAX_LOOPS) seq |= ~0ull << (8 * n);  // unused positions 0xFF
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j) d.order[j] = (uint8_t)(seq >> (8 * j));
+  // codes outside the space decode to an illegal record (n_loops 0), which
+  // the featurizer reports as TS_ERR_ILLEGAL
+  const bool bad = (code >> 11) != 0u || sc0 == 3u || sc1 == 3u || (np < 2 && sc1 != 0u) || np < 1 ||
+                   n > TS_MAX_LOOPS;
+  d.n_loops = bad ? 0 : (uint8_t)n;
+  d.vec = ((code >> 8) & 1u) ? 8 : 1;
+  d.flags = (uint8_t)(((code >> 9) & 1u) | (((code >> 10) & 1u) << 1));
+  d.anchor = (int8_t)((int)(code & 3u) - 1);
+  return d;
+}
+
 // check_action (schedule_space.py:288-347) on an encoded decision: null if
 // legal, else the violated invariant.  Host only.
 inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const Nest* cn,

@@ -238,6 +238,7 @@ struct TcArgs {
   int record_prefix;
   double target_scale;
   double b_out;
+  int* tile_counter;        // zeroed before the launch: dynamic tile scheduler (null: static)
 };
 
 // x at timestep t: intrinsic half from the stage's init row (the same for
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   float* wout = reinterpret_cast<float*>(smem + (1 + NWG) * TILE_BYTES);  // [32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(wout + 64);               // [NWG]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
+  volatile int* tile_slot = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [NWG]
 
   // weights -> shared (B' image is already in the canonical layout)
   {
@@ -295,7 +297,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   const float c2 = -2.0f * LOG2E;
   put_bias_ones(A, r);
 
-  for (int tile = blockIdx.x * NWG + wg; tile < a.n_tiles; tile += gridDim.x * NWG) {
+  // Tiles are in descending depth order; each warpgroup starts with one of
+  // the first gridDim*NWG and then takes the next unclaimed tile (longest
+  // first, so the short tail tiles fill the gaps)
+  for (int tile = blockIdx.x * NWG + wg; tile < a.n_tiles;) {
     const int64_t sp = (int64_t)tile * TM + r;
     const bool valid = a.record_prefix ? (r == 0) : (sp < a.n);
     int64_t st = 0, off = 0;
@@ -399,7 +404,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       fence_before();  // TMEM reads complete before the next UMMA overwrites D
     }
     if (!a.record_prefix && valid) a.out[st] = exp(fadd(raw, a.target_scale));
-    wg_sync(wg);
+    if (a.tile_counter) {
+      if (r == 0) tile_slot[wg] = gridDim.x * NWG + atomicAdd(a.tile_counter, 1);
+      wg_sync(wg);
+      tile = tile_slot[wg];
+    } else {
+      wg_sync(wg);
+      tile += gridDim.x * NWG;
+    }
   }
   fence_before();
   __syncthreads();

@@ -255,6 +255,85 @@ def encode_states(states):
     return out
 
 
+# ------------------------------------------------------- action codes
+# 16-bit codes of decisions in candidate_actions' space (layout:
+# include/tensched_b200.h, ts_score_states_coded).
+_SPLIT_CODE = np.full(256, 255, dtype=np.uint8)
+_SPLIT_CODE[[0, 8, 32]] = [0, 1, 2]
+
+
+def _order_variants(st, split_mask):
+    """The four (placement, swap) orders of _order_options (schedule_space.py
+    :361-376) as loop-id bytes packed little-endian into a u64, for a stage
+    whose splittable dims are split per `split_mask` (bit 0: dims[-2:][0])."""
+    n_pure, n_red = len(st.dims), len(st.reduction_dims)
+    first = n_pure - 2 if n_pure >= 2 else 0
+    pure = []
+    for k in range(n_pure):
+        pure.append(2 * k)
+        if first <= k < first + 2 and (split_mask >> (k - first)) & 1:
+            pure.append(2 * k + 1)
+    red = [8 + r for r in range(n_red)]
+    out = []
+    for outer in (0, 1):
+        for swap in (0, 1):
+            seq = (red + pure) if outer else (pure + red)
+            if swap and len(seq) >= 2:
+                seq = seq[:-2] + [seq[-1], seq[-2]]
+            if len(seq) > 8:
+                out.append(None)
+                continue
+            b = bytes(seq) + b"\xff" * (8 - len(seq))
+            out.append(int.from_bytes(b, "little"))
+    return out
+
+
+def action_codes(inf, recs, offsets):
+    """Decision records (schedule order per state) -> u16 action codes, or None
+    when some decision lies outside candidate_actions' space."""
+    n = len(recs)
+    if n == 0:
+        return np.zeros(0, dtype=np.uint16)
+    depths = np.diff(offsets)
+    pos = np.arange(n, dtype=np.int64) - np.repeat(offsets[:-1], depths)
+    n_pure = np.array([len(st.dims) for st in inf.stages], dtype=np.int64)[pos]
+    first = np.where(n_pure >= 2, n_pure - 2, 0)
+    split = recs["split"].astype(np.int64)
+    sc = _SPLIT_CODE[recs["split"]]
+    rows = np.arange(n)
+    s0 = sc[rows, first]
+    s1 = np.where(n_pure >= 2, sc[rows, np.minimum(first + 1, 3)], 0)
+    # splits only on the splittable dims, by SPLIT_FACTORS
+    kk = np.arange(4)[None, :]
+    other = (kk != first[:, None]) & ((kk != first[:, None] + 1) | (n_pure[:, None] < 2))
+    if np.any(split[other] != 0) or np.any(s0 == 255) or np.any(s1 == 255):
+        return None
+    anchor = recs["anchor"].astype(np.int64)
+    vec = recs["vec"].astype(np.int64)
+    flags = recs["flags"].astype(np.int64)
+    if np.any((anchor < -1) | (anchor > 2)) or np.any((vec != 1) & (vec != 8)) or np.any(flags > 3):
+        return None
+    order = np.ascontiguousarray(recs["order"]).view("<u8").ravel()
+    mask = (s0 != 0).astype(np.int64) | ((s1 != 0).astype(np.int64) << 1)
+    key = pos * 4 + mask
+    ob = np.full(n, -1, dtype=np.int64)
+    for k in np.unique(key):
+        sel = key == k
+        st = inf.stages[int(k) // 4]
+        got = order[sel]
+        bits = np.full(got.shape, -1, dtype=np.int64)
+        for v, want in enumerate(_order_variants(st, int(k) % 4)):
+            if want is not None:
+                bits = np.where((bits < 0) & (got == np.uint64(want)), v, bits)
+        ob[sel] = bits
+    if np.any(ob < 0):
+        return None
+    outer, swap = ob >> 1, ob & 1
+    code = ((anchor + 1) | (s0.astype(np.int64) << 2) | (s1.astype(np.int64) << 4) | (outer << 6) | (swap << 7)
+            | ((vec == 8).astype(np.int64) << 8) | ((flags & 1) << 9) | (((flags >> 1) & 1) << 10))
+    return code.astype(np.uint16)
+
+
 def _host_ctx():
     """Context for host-side library calls (enumeration/legality): the device
     context when a GPU is present, else a host-only context."""

@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from .errors import CheckpointError, PipelineError
 from .featurizer import FEATURE_WIDTH, Normalizer
-from .schedule_space import encode_states
+from .schedule_space import action_codes, encode_states
 
 INPUT_DIM = FEATURE_WIDTH
 PACKED_MIN = 4096  # batches at least this large travel in the 8-byte wire format
@@ -80,9 +80,15 @@ def predict_states(params, states, jobs: int = 1, mode: int = MODE_EXACT, device
     for inf, idxs, recs, offsets in encode_states(states):
         pid = ctx.pipeline_id(inf.desc)
         vals = np.empty(len(idxs))
-        packed = _lib.pack_records(recs) if len(idxs) >= PACKED_MIN and inf.T < 256 else None
+        big = len(idxs) >= PACKED_MIN and inf.T < 256
+        codes = action_codes(inf, recs, offsets) if big else None
+        packed = _lib.pack_records(recs) if big and codes is None else None
         with ctx.lock:
-            if packed is not None:  # half the PCIe bytes (ts_score_states_packed)
+            if codes is not None:  # 2 bytes per decision (ts_score_states_coded)
+                depths = np.diff(offsets).astype(np.uint8)
+                ctx.check(ctx.lib.ts_score_states_coded(ctx.h, pid, _lib._p(codes), _lib._p(depths),
+                                                        len(idxs), int(mode), _lib._p(vals)))
+            elif packed is not None:  # 8 bytes per decision (ts_score_states_packed)
                 depths = np.diff(offsets).astype(np.uint8)
                 ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, _lib._p(packed), _lib._p(depths),
                                                          len(idxs), int(mode), _lib._p(vals)))

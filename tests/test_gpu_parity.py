@@ -210,3 +210,50 @@ def test_packed_wire_format_matches(state_sets, v0):
             ctx.check(ctx.lib.ts_score_states_packed(ctx.h, pid, _lib._p(packed), _lib._p(depths),
                                                      len(idxs), mode, _lib._p(b)))
             assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.gpu
+def test_coded_wire_format_matches(gpu_ctx, v0):
+    """ts_score_states_coded (16-bit action codes decoded in the featurizer +
+    u8 depths) == ts_score_states on 2e5 device-generated VGG-16 states, both
+    modes, bit for bit; several chunkings; an out-of-space code is reported."""
+    import ctypes
+    import os
+    import torch
+    from paper_2011_14486_b200 import _lib
+    p = pipeline_from({"text": (__import__("pathlib").Path(__file__).resolve().parent.parent
+                                / "assets/pipelines/nets/vgg16.pl").read_text()})
+    inf = ss._info(p)
+    pid = gpu_ctx.pipeline_id(inf.desc)
+    gpu_ctx.set_params(v0)
+    n = 200_000
+    recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
+    offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    nrec = ctypes.c_int64()
+    gpu_ctx.check(gpu_ctx.lib.ts_generate_states_device(gpu_ctx.h, pid, 4242, n, recs.data_ptr(),
+                                                        offs.data_ptr(), ctypes.byref(nrec)))
+    h_recs = np.frombuffer(recs[: nrec.value * 16].cpu().numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
+    h_offs = offs.cpu().numpy()
+    codes = ss.action_codes(inf, h_recs, h_offs)
+    assert codes is not None
+    depths = np.diff(h_offs).astype(np.uint8)
+    for mode in (MODE_EXACT, MODE_FAST):
+        a = np.empty(n)
+        gpu_ctx.check(gpu_ctx.lib.ts_score_states(gpu_ctx.h, pid, _lib._p(h_recs), _lib._p(h_offs), n, mode,
+                                                  _lib._p(a)))
+        for chunk in (None, "50000"):
+            if chunk:
+                os.environ["TS_CODED_CHUNK"] = chunk
+            b = np.empty(n)
+            try:
+                gpu_ctx.check(gpu_ctx.lib.ts_score_states_coded(gpu_ctx.h, pid, _lib._p(codes), _lib._p(depths),
+                                                                n, mode, _lib._p(b)))
+            finally:
+                os.environ.pop("TS_CODED_CHUNK", None)
+            assert np.array_equal(bits(a), bits(b)), (mode, chunk)
+    bad = codes.copy()
+    bad[5] = 0xF800  # reserved bits set
+    b = np.empty(n)
+    rc = gpu_ctx.lib.ts_score_states_coded(gpu_ctx.h, pid, _lib._p(bad), _lib._p(depths), n, MODE_FAST,
+                                           _lib._p(b))
+    assert rc != 0

@@ -76,6 +76,42 @@ def test_encode_decode_roundtrip(state_sets):
                 assert [d.render() for d in dec] == [d.render() for d in states[i].decisions]
 
 
+def test_action_codes_roundtrip_every_candidate(candidates_golden, greedy_golden):
+    """Every decision candidate_actions produces along the golden walks has a
+    16-bit action code, and the native decoder (the featurizer's) turns the
+    codes back into the identical 16-byte records."""
+    ctx = _lib.host_context()
+    for key, walk in candidates_golden.items():
+        p = pipeline_from(greedy_golden[key])
+        s = ss.initial_state(p)
+        r5 = __import__("oracle").SplitMix(5)
+        children = []
+        for _ in walk:
+            c = ss.candidate_actions(s)
+            children += [ss.apply(s, a) for a in c]
+            s = ss.apply(s, c[r5.randrange(len(c))])
+        for inf, idxs, recs, offs in ss.encode_states(children):
+            codes = ss.action_codes(inf, recs, offs)
+            assert codes is not None, key
+            depths = np.diff(offs).astype(np.uint8)
+            out = np.zeros(len(recs), dtype=_lib.DECISION_DTYPE)
+            pid = ctx.pipeline_id(inf.desc)
+            ctx.check(ctx.lib.ts_decode_codes(ctx.h, pid, _lib._p(codes), _lib._p(depths), len(idxs),
+                                              _lib._p(out)))
+            assert out.tobytes() == recs.tobytes(), key
+
+
+def test_action_codes_reject_decisions_outside_the_space(greedy_golden):
+    p = pipeline_from(greedy_golden["ref:pipelines/toys/t2_stencil.pl"])
+    s0 = ss.initial_state(p)
+    name = ss._info(p).sched[0]
+    for odd in (ss.LayerSchedule(name, (("x", 4),), ("xo", "xi")),   # factor outside SPLIT_FACTORS
+                ss.LayerSchedule(name, (), ("x",), 4)):               # width outside VEC_WIDTHS
+        assert ss.check_action(s0, odd) is None
+        [(inf, idxs, recs, offs)] = ss.encode_states([ss.apply(s0, odd)])
+        assert ss.action_codes(inf, recs, offs) is None
+
+
 def test_check_action_rejects_illegal(greedy_golden):
     p = pipeline_from(greedy_golden["ref:pipelines/toys/t2_stencil.pl"])
     s = ss.initial_state(p)
