@@ -162,6 +162,10 @@ __device__ __forceinline__ float rcp_fma(float d) {
   return r;
 }
 
+#ifndef TS_PAIR_RCP
+#define TS_PAIR_RCP 1  // pairwise shared reciprocals (6 MUFU ops per unit instead of 7)
+#endif
+
 #ifndef TS_FMA_RCP
 #define TS_FMA_RCP 0  // how many of the 2 per-unit reciprocals use rcp_fma (0..2)
 #endif
@@ -370,6 +374,44 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
         tmem_ld8(lane_addr + 3 * 32 + g8 * 8, uo);
         tmem_wait_ld();
         float h8[8];
+#if TS_PAIR_RCP
+        // Units in pairs share each reciprocal (Montgomery's batch
+        // inversion: 1/a = b/(ab), 1/b = a/(ab)), 6 MUFU ops per unit: the
+        // denominators are pre-scaled through the FMA constants (t_i by
+        // 2^-60, 1 + e_o by 2^-40, exact) so the pair products stay inside
+        // [2^-120, 2^120] with the exponents clamped at 40.
+        constexpr float S1 = 8.673617379884035e-19f;  // 2^-60
+        constexpr float S2 = 9.094947017729282e-13f;  // 2^-40
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          float tig[2], num[2], d1[2], eo[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int uu = u + q, j = g8 * 8 + uu;
+            const float ei = ex2(clamp40(ui[uu])), ef = ex2(clamp40(uf[uu]));
+            const float eg = ex2(clamp40(vg[uu]));
+            eo[q] = ex2(clamp40(uo[uu]));
+            const float tf = 1.0f + ef;
+            tig[q] = fmaf(ei, S1, S1) * (1.0f + eg);          // 2^-60 t_i t_g
+            num[q] = fmaf(c[j], tig[q], fmaf(-eg, S1, S1) * tf);  // 2^-60 (c t_i t_g + (1 - e_g) t_f)
+            d1[q] = tf * tig[q];                               // 2^-60 t_f t_i t_g
+          }
+          const float r1 = rcp(d1[0] * d1[1]);
+          c[g8 * 8 + u] = num[0] * (d1[1] * r1);
+          c[g8 * 8 + u + 1] = num[1] * (d1[0] * r1);
+          float ec[2], d2[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            ec[q] = ex2(clamp40(c2 * c[g8 * 8 + u + q]));
+            d2[q] = fmaf(eo[q], S2, S2) * (1.0f + ec[q]);     // 2^-40 (1 + e_o)(1 + e_c)
+          }
+          const float r2 = rcp(d2[0] * d2[1]);
+          h8[u] = fmaf(-ec[0], S2, S2) * (d2[1] * r2);
+          h8[u + 1] = fmaf(-ec[1], S2, S2) * (d2[0] * r2);
+          acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
+          acc = fmaf(h8[u + 1], wout[g8 * 8 + u + 1], acc);
+        }
+#else
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           // With t_x = 1 + 2^u_x:  sigma = 1/t,  tanh = (1 - 2^v)/(1 + 2^v), so
@@ -389,6 +431,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           h8[u] = (1.0f - ec) * rcp_sel((1.0f + eo) * (1.0f + ec), 1);
           acc = fmaf(h8[u], wout[j], acc);
         }
+#endif
         // the UMMA that read A has completed (mbarrier), so h can go straight in
         put_h8(A, r, g8, h8);
         if (prow) {
