@@ -878,18 +878,21 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     rc = ensure_fast_prefix(ctx, P);
     if (rc) return rc;
   }
-  // codes are 1/8 of the record bytes, so two chunks hide the transfer
-  int64_t chunk = std::max<int64_t>(1 << 16, (n_states + 1) / 2);
-  if (const char* e = getenv("TS_CODED_CHUNK")) chunk = std::max<int64_t>(1024, atoll(e));
-  if (chunk > n_states) chunk = n_states;
-  const int64_t n_chunks = (n_states + chunk - 1) / chunk;
+  // Codes are 1/8 of the record bytes: a first chunk of a quarter of the
+  // states starts the device while the rest is in flight, and the rest runs
+  // as one batch (full-size launches keep their efficiency).
+  int64_t first = n_states >= (1 << 18) ? n_states / 4 : n_states;
+  if (const char* e = getenv("TS_CODED_CHUNK")) first = std::max<int64_t>(1024, atoll(e));
+  if (first > n_states) first = n_states;
+  std::vector<int64_t> st_at = {0, first};
+  if (first < n_states) st_at.push_back(n_states);
+  const int64_t n_chunks = (int64_t)st_at.size() - 1;
   std::vector<int64_t> rec_at(n_chunks + 1);
   {
     int64_t acc = 0;
     for (int64_t k = 0; k < n_chunks; ++k) {
       rec_at[k] = acc;
-      const int64_t s1 = std::min(n_states, (k + 1) * chunk);
-      acc += (int64_t)sum_bytes(depths + k * chunk, s1 - k * chunk);
+      acc += (int64_t)sum_bytes(depths + st_at[k], st_at[k + 1] - st_at[k]);
     }
     rec_at[n_chunks] = acc;
   }
@@ -933,7 +936,7 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     ++ctx->launches;
   }
   for (int64_t k = 0; k < n_chunks; ++k) {
-    const int64_t s0 = k * chunk, s1 = std::min(n_states, s0 + chunk);
+    const int64_t s0 = st_at[k], s1 = st_at[k + 1];
     TS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k + 1], 0));
     rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, n_rec, mode,
                       ctx->out.as<double>() + s0, d_codes);

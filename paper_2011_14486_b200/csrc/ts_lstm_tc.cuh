@@ -388,9 +388,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int uu = u + q, j = g8 * 8 + uu;
-            const float ei = ex2(clamp40(ui[uu])), ef = ex2(clamp40(uf[uu]));
-            const float eg = ex2(clamp40(vg[uu]));
-            eo[q] = ex2(clamp40(uo[uu]));
+            const float ei = ex2_sel(clamp40(ui[uu]), 0), ef = ex2_sel(clamp40(uf[uu]), 1);
+            const float eg = ex2_sel(clamp40(vg[uu]), 2);
+            eo[q] = ex2_sel(clamp40(uo[uu]), 3);
             const float tf = 1.0f + ef;
             tig[q] = fmaf(ei, S1, S1) * (1.0f + eg);          // 2^-60 t_i t_g
             num[q] = fmaf(c[j], tig[q], fmaf(-eg, S1, S1) * tf);  // 2^-60 (c t_i t_g + (1 - e_g) t_f)
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           float ec[2], d2[2];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            ec[q] = ex2(clamp40(c2 * c[g8 * 8 + u + q]));
+            ec[q] = ex2_sel(clamp40(c2 * c[g8 * 8 + u + q]), 4);
             d2[q] = fmaf(eo[q], S2, S2) * (1.0f + ec[q]);     // 2^-40 (1 + e_o)(1 + e_c)
           }
           const float r2 = rcp(d2[0] * d2[1]);

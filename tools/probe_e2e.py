@@ -73,7 +73,7 @@ print(f"bare H2D {h_packed.numel() * 8 / 1e6:.0f} MB          {timed(lambda: d_b
 from paper_2011_14486_b200.schedule_space import action_codes  # noqa: E402
 codes = action_codes(inf, np.frombuffer(h_recs.tobytes(), dtype=_lib.DECISION_DTYPE), h_offs)
 h_codes = torch.from_numpy(codes.view(np.int16)).pin_memory()
-for chunk in (1 << 20, 1 << 19, 1 << 18, 1 << 17):
+for chunk in (1 << 20, 1 << 19, 1 << 18, 1 << 17, 1 << 16):
     os.environ["TS_CODED_CHUNK"] = str(chunk)
 
     def coded():
