@@ -434,9 +434,9 @@ def main():
     dom = max(avg, key=lambda k: times[names.index(k)])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     # ncu --set full capture (profiles/r01_ncu.md): DRAM bytes per state of each
-    # kernel at 262,144 states, scaled to this launch
-    traffic_per_state = {"featurize": (100.080128e6 + 368.331776e6) / 262144,
-                         "lstm_fast": (309.275648e6 + 4.245760e6) / 262144}
+    # kernel at 2^20 states, scaled to this launch
+    traffic_per_state = {"featurize": (449.214208e6 + 572.307200e6) / 1048576,
+                         "lstm_fast": (633.981696e6 + 17.002240e6) / 1048576}
     row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
         bytes_per_launch = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
@@ -458,8 +458,9 @@ def main():
                 "traffic": tr * M if tr else None, "flops_per_launch": flops_per_launch,
                 "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
     roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
-    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU-bound (XU pipe 89% "
-                    "in ncu), k_featurize_rows is issue/divergence-bound (profiles/r01_ncu.md)")
+    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 76%, "
+                    "issue 64% in ncu), k_featurize_rows is ALU/issue-bound integer work (ALU 50%, issue 61%); "
+                    "profiles/r01_ncu.md")
 
     train_line = None
     if not args.no_train:
