@@ -563,12 +563,9 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   if (P->fast_version == ctx->params_version) return TS_OK;
   const int T = P->h->n_stages;
   TS_CUDA(P->pre_fast.reserve(fast_pre_bytes(T) + sizeof(float) * T * F));
-  float* init32 = reinterpret_cast<float*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
-  {
-    const int64_t nw = (int64_t)T * F;
-    tc::k_rows32<<<(unsigned)((nw + 255) / 256), 256, 0, ctx->stream>>>(P->init_norm.as<double>(), nw, init32);
-    TS_LAUNCHED();
-  }
+  uint4* initx = reinterpret_cast<uint4*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
+  tc::k_init_split<<<(unsigned)((T + 63) / 64), 64, 0, ctx->stream>>>(P->init_norm.as<double>(), T, initx);
+  TS_LAUNCHED();
   if (!ctx->tc_attr_set) {
     TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
     ctx->tc_attr_set = true;
@@ -576,7 +573,7 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   tc::TcArgs ta;
   memset(&ta, 0, sizeof ta);
   ta.wpack = ctx->fast_w.as<uint8_t>();
-  ta.init32 = init32;
+  ta.initx = initx;
   ta.pre = P->pre_fast.as<float>();
   ta.T = T;
   ta.n_tiles = 1;
@@ -650,8 +647,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     }
     tc::TcArgs ta;
     ta.wpack = ctx->fast_w.as<uint8_t>();
-    ta.init32 = reinterpret_cast<const float*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
-    ta.rows32 = ctx->rows.as<float>();
+    ta.initx = reinterpret_cast<const uint4*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
+    ta.rowsx = ctx->rows.as<uint4>();
     ta.offsets = d_offsets;
     ta.perm = perm;
     ta.rowoff = rowoff;

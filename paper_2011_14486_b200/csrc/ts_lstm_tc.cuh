@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include "ts_core.cuh"
+#include "ts_f16.cuh"
 
 namespace ts {
 namespace tc {
@@ -173,35 +174,19 @@ __device__ __forceinline__ float rcp_sel(float x, int slot) {
   return slot < TS_FMA_RCP ? rcp_fma(x) : rcp(x);
 }
 
-// hi/lo fp16 split of 8 floats into two 16-byte chunks
-__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
-  uint32_t h[4], l[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __half2 hh = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-    const float2 back = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(v[2 * i] - back.x, v[2 * i + 1] - back.y);
-    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
-    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
-  }
-  hi = make_uint4(h[0], h[1], h[2], h[3]);
-  lo = make_uint4(l[0], l[1], l[2], l[3]);
-}
-
 // Stores 16-byte chunk `kc` of row `r` in the canonical no-swizzle layout.
 __device__ __forceinline__ void st_chunk(uint8_t* A, int kc, int r, const uint4& v) {
   *reinterpret_cast<uint4*>(A + kc * CHUNK_STRIDE + (r >> 3) * 128 + (r & 7) * 16) = v;
 }
 
-// x part: chunks q = 0, 1 of every segment
-__device__ __forceinline__ void put_x(uint8_t* A, int r, const float* x) {
+// x part, pre-split (x4 = intrinsic hi, lo, acquired hi, lo): chunks q = 0
+// (intrinsic), 1 (acquired) of every segment
+__device__ __forceinline__ void put_x(uint8_t* A, int r, const uint4* x4) {
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
-    uint4 hi, lo;
-    split8(x + 8 * q, hi, lo);
-    st_chunk(A, 0 * 6 + q, r, hi);
-    st_chunk(A, 1 * 6 + q, r, lo);
-    st_chunk(A, 2 * 6 + q, r, hi);
+    st_chunk(A, 0 * 6 + q, r, x4[2 * q]);
+    st_chunk(A, 1 * 6 + q, r, x4[2 * q + 1]);
+    st_chunk(A, 2 * 6 + q, r, x4[2 * q]);
   }
 }
 
@@ -229,8 +214,8 @@ __device__ __forceinline__ void put_bias_ones(uint8_t* A, int r) {
 // writes (h, c, raw) before every timestep into `pre` (the fast prefix).
 struct TcArgs {
   const uint8_t* wpack;     // B' image (TILE_BYTES) + readout w[32] f32
-  const float* init32;      // [T][16] normalized unscheduled rows (fp32)
-  const float* rows32;      // [n_records][8] normalized acquired features of scheduled rows (fp32)
+  const uint4* initx;       // [T][4] unscheduled rows, split fp16: intrinsic hi, lo, acquired hi, lo
+  const uint4* rowsx;       // [n_records][2] acquired half of scheduled rows, split fp16: hi, lo
   const int64_t* offsets;   // [n+1]
   const int* perm;          // [n] sorted position -> state
   const int64_t* rowoff;    // [T+1] decision-major row offsets (k_depth_scan)
@@ -247,15 +232,12 @@ struct TcArgs {
 
 // x at timestep t: intrinsic half from the stage's init row (the same for
 // every row of the tile), acquired half from the init row (unscheduled) or
-// the state's scheduled row
-__device__ __forceinline__ void load_x(const float* init_row, const float* acq, float* x) {
-  const float4* i4 = reinterpret_cast<const float4*>(init_row);
-  const float4* a4 = reinterpret_cast<const float4*>(acq);
-  const float4 v0 = __ldg(i4), v1 = __ldg(i4 + 1), v2 = __ldg(a4), v3 = __ldg(a4 + 1);
-  x[0] = v0.x, x[1] = v0.y, x[2] = v0.z, x[3] = v0.w;
-  x[4] = v1.x, x[5] = v1.y, x[6] = v1.z, x[7] = v1.w;
-  x[8] = v2.x, x[9] = v2.y, x[10] = v2.z, x[11] = v2.w;
-  x[12] = v3.x, x[13] = v3.y, x[14] = v3.z, x[15] = v3.w;
+// the state's scheduled row; both already split into fp16 hi/lo
+__device__ __forceinline__ void load_x(const uint4* init_row, const uint4* acq, uint4* x4) {
+  x4[0] = __ldg(init_row);
+  x4[1] = __ldg(init_row + 1);
+  x4[2] = __ldg(acq);
+  x4[3] = __ldg(acq + 1);
 }
 
 __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
@@ -340,9 +322,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
 #pragma unroll
       for (int g8 = 0; g8 < 4; ++g8) put_h8(A, r, g8, h0 + 8 * g8);
     }
-    float x[16];
-    load_x(a.init32 + t0 * 16, (t0 < T - d) ? a.init32 + t0 * 16 + 8 : a.rows32 + (a.rowoff[T - 1 - t0] + sp) * 8,
-           x);
+    uint4 x[4];
+    load_x(a.initx + t0 * 4, (t0 < T - d) ? a.initx + t0 * 4 + 2 : a.rowsx + (a.rowoff[T - 1 - t0] + sp) * 2, x);
     for (int t = t0; t < T; ++t) {
       put_x(A, r, x);
       fence_async_smem();
@@ -358,8 +339,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       }
       // prefetch the next row while the tensor core works
       if (t + 1 < T)
-        load_x(a.init32 + (t + 1) * 16,
-               (t + 1 < T - d) ? a.init32 + (t + 1) * 16 + 8 : a.rows32 + (a.rowoff[T - 2 - t] + sp) * 8, x);
+        load_x(a.initx + (t + 1) * 4,
+               (t + 1 < T - d) ? a.initx + (t + 1) * 4 + 2 : a.rowsx + (a.rowoff[T - 2 - t] + sp) * 2, x);
       mbar_wait(bar, phase);
       phase ^= 1u;
       fence_after();
@@ -471,10 +452,16 @@ __global__ void k_prefix0(float* pre, int T, double b_out) {
   if (j == 0) *reinterpret_cast<double*>(pre + 64) = fmul((double)T, b_out);
 }
 
-// --------------------------------------------- featurize -> fp32 rows
-__global__ void k_rows32(const double* __restrict__ rows64, int64_t n_words, float* __restrict__ rows32) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_words) rows32[i] = (float)rows64[i];
+// --------------------------------------------- unscheduled rows -> split fp16
+// initx[t] = {hi, lo} of (float) init_norm[t][0..7] and of [8..15]
+__global__ void k_init_split(const double* __restrict__ init_norm, int T, uint4* __restrict__ initx) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = (float)init_norm[t * 16 + k];
+  split8(v, initx[4 * t], initx[4 * t + 1]);
+  split8(v + 8, initx[4 * t + 2], initx[4 * t + 3]);
 }
 
 // --------------------------------------------- depth bucketing (counting sort)
