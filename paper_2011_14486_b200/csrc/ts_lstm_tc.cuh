@@ -150,30 +150,6 @@ __device__ __forceinline__ float ex2_sel(float x, int slot) {
   return slot < TS_FMA_EXP ? ex2_fma(x) : ex2(x);
 }
 
-// 1/d on the FMA pipe for d in [1, 2^126): integer seed (|rel err| < 1/8)
-// and two cubic Newton steps r += r*(e + e^2), e = 1 - d*r (error ~1e-9
-// before rounding, i.e. within 1-2 ulp like rcp.approx).
-__device__ __forceinline__ float rcp_fma(float d) {
-  float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const float e = fmaf(-d, r, 1.0f);
-    r = fmaf(r, fmaf(e, e, e), r);
-  }
-  return r;
-}
-
-#ifndef TS_PAIR_RCP
-#define TS_PAIR_RCP 1  // pairwise shared reciprocals (6 MUFU ops per unit instead of 7)
-#endif
-
-#ifndef TS_FMA_RCP
-#define TS_FMA_RCP 0  // how many of the 2 per-unit reciprocals use rcp_fma (0..2)
-#endif
-__device__ __forceinline__ float rcp_sel(float x, int slot) {
-  return slot < TS_FMA_RCP ? rcp_fma(x) : rcp(x);
-}
-
 // Stores 16-byte chunk `kc` of row `r` in the canonical no-swizzle layout.
 __device__ __forceinline__ void st_chunk(uint8_t* A, int kc, int r, const uint4& v) {
   *reinterpret_cast<uint4*>(A + kc * CHUNK_STRIDE + (r >> 3) * 128 + (r & 7) * 16) = v;
@@ -280,7 +256,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   uint64_t* bar = bars + wg;
   uint32_t phase = 0;
   const int T = a.T;
-  const float c2 = -2.0f * LOG2E;
   put_bias_ones(A, r);
 
   // Tiles are in descending depth order; each warpgroup starts with one of
@@ -355,14 +330,18 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
         tmem_ld8(lane_addr + 3 * 32 + g8 * 8, uo);
         tmem_wait_ld();
         float h8[8];
-#if TS_PAIR_RCP
+        // Fused cell algebra.  With t_x = 1 + 2^u_x: sigma = 1/t and
+        // tanh = (1 - 2^v)/(1 + 2^v), so
+        //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
+        //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c)).
         // Units in pairs share each reciprocal (Montgomery's batch
-        // inversion: 1/a = b/(ab), 1/b = a/(ab)), 6 MUFU ops per unit: the
-        // denominators are pre-scaled through the FMA constants (t_i by
+        // inversion: 1/a = b/(ab), 1/b = a/(ab)): 5 ex2 + 1 rcp per unit.
+        // The denominators are pre-scaled through the FMA constants (t_i by
         // 2^-60, 1 + e_o by 2^-40, exact) so the pair products stay inside
-        // [2^-120, 2^120] with the exponents clamped at 40.
+        // [2^-120, 2^120] with the exponents clamped at 40 (sigma >= 2^-40).
         constexpr float S1 = 8.673617379884035e-19f;  // 2^-60
         constexpr float S2 = 9.094947017729282e-13f;  // 2^-40
+        constexpr float C2 = -2.0f * LOG2E;
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
           float tig[2], num[2], d1[2], eo[2];
@@ -383,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           float ec[2], d2[2];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            ec[q] = ex2_sel(clamp40(c2 * c[g8 * 8 + u + q]), 4);
+            ec[q] = ex2_sel(clamp40(C2 * c[g8 * 8 + u + q]), 4);
             d2[q] = fmaf(eo[q], S2, S2) * (1.0f + ec[q]);     // 2^-40 (1 + e_o)(1 + e_c)
           }
           const float r2 = rcp(d2[0] * d2[1]);
@@ -392,27 +371,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
           acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
           acc = fmaf(h8[u + 1], wout[g8 * 8 + u + 1], acc);
         }
-#else
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          // With t_x = 1 + 2^u_x:  sigma = 1/t,  tanh = (1 - 2^v)/(1 + 2^v), so
-          //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
-          //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c))
-          // 5 ex2 + 2 rcp per unit instead of 5 + 5.  Exponents are clamped
-          // above at 40 (sigma(z) >= 2^-40 instead of smaller) so the
-          // products stay finite in fp32.
-          const int j = g8 * 8 + u;
-          const float ei = ex2_sel(clamp40(ui[u]), 0), ef = ex2_sel(clamp40(uf[u]), 1);
-          const float eg = ex2_sel(clamp40(vg[u]), 2), eo = ex2_sel(clamp40(uo[u]), 3);
-          const float ti = 1.0f + ei, tf = 1.0f + ef, tg = 1.0f + eg;
-          const float tig = ti * tg;
-          const float num = fmaf(c[j], tig, (1.0f - eg) * tf);
-          c[j] = num * rcp_sel(tf * tig, 0);
-          const float ec = ex2_sel(clamp40(c2 * c[j]), 4);
-          h8[u] = (1.0f - ec) * rcp_sel((1.0f + eo) * (1.0f + ec), 1);
-          acc = fmaf(h8[u], wout[j], acc);
-        }
-#endif
         // the UMMA that read A has completed (mbarrier), so h can go straight in
         put_h8(A, r, g8, h8);
         if (prow) {
