@@ -351,10 +351,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
             const float ei = ex2_sel(clamp40(ui[uu]), 0), ef = ex2_sel(clamp40(uf[uu]), 1);
             const float eg = ex2_sel(clamp40(vg[uu]), 2);
             eo[q] = ex2_sel(clamp40(uo[uu]), 3);
-            const float tf = 1.0f + ef;
-            tig[q] = fmaf(ei, S1, S1) * (1.0f + eg);          // 2^-60 t_i t_g
-            num[q] = fmaf(c[j], tig[q], fmaf(-eg, S1, S1) * tf);  // 2^-60 (c t_i t_g + (1 - e_g) t_f)
-            d1[q] = tf * tig[q];                               // 2^-60 t_f t_i t_g
+            // products by (1 + e) as fused a + a e: t_f is never formed
+            const float ti = fmaf(ei, S1, S1);                 // 2^-60 t_i
+            tig[q] = fmaf(ti, eg, ti);                         // 2^-60 t_i t_g
+            const float gm = fmaf(-eg, S1, S1);                // 2^-60 (1 - e_g)
+            num[q] = fmaf(c[j], tig[q], fmaf(gm, ef, gm));     // 2^-60 (c t_i t_g + (1 - e_g) t_f)
+            d1[q] = fmaf(tig[q], ef, tig[q]);                  // 2^-60 t_f t_i t_g
           }
           const float r1 = rcp(d1[0] * d1[1]);
           c[g8 * 8 + u] = num[0] * (d1[1] * r1);
@@ -363,7 +365,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             ec[q] = ex2_sel(clamp40(C2 * c[g8 * 8 + u + q]), 4);
-            d2[q] = fmaf(eo[q], S2, S2) * (1.0f + ec[q]);     // 2^-40 (1 + e_o)(1 + e_c)
+            const float to = fmaf(eo[q], S2, S2);             // 2^-40 (1 + e_o)
+            d2[q] = fmaf(to, ec[q], to);                       // 2^-40 (1 + e_o)(1 + e_c)
           }
           const float r2 = rcp(d2[0] * d2[1]);
           h8[u] = fmaf(-ec[0], S2, S2) * (d2[1] * r2);
