@@ -106,6 +106,7 @@ struct ts_ctx {
   int64_t launches = 0;
   int sm_count = 148;
   bool tc_attr_set = false;
+  bool exact_attr_set = false;
   // optional per-kernel-class timing (bench.py): events around launches on
   // the context stream, resolved at the next host synchronization
   bool timing = false;
@@ -607,9 +608,23 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     {
       const int64_t threads = n_states * 32;
       KTimer kt(ctx, TS_K_LSTM_EXACT);
-      k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
-          lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
-          ctx->target_scale, d_out);
+      if (ctx->hidden == 32) {
+        // 16 warps per block share one copy of the weights in shared memory
+        if (!ctx->exact_attr_set) {
+          TS_CUDA(cudaFuncSetAttribute(k_score_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(ExactSmem)));
+          TS_CUDA(cudaFuncSetAttribute(k_children_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(ExactSmem)));
+          ctx->exact_attr_set = true;
+        }
+        k_score_exact32<<<(unsigned)((threads + 511) / 512), 512, sizeof(ExactSmem), ctx->stream>>>(
+            lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
+            ctx->target_scale, d_out);
+      } else {
+        k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
+            lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
+            ctx->target_scale, d_out);
+      }
       TS_LAUNCHED();
     }
     return TS_OK;
@@ -1136,9 +1151,23 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     TS_LAUNCHED();
     k_dedup<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
     TS_LAUNCHED();
-    k_children_exact<<<(n * 32 + 127) / 128, 128, 0, ctx->stream>>>(
-        lstm_weights(ctx), P->pre_exact.as<double>(), T, s, ctx->rows.as<double>(), ctx->reps.as<int>(), n,
-        state_rows, ctx->raw.as<double>());
+    if (ctx->hidden == 32) {
+      // a few warps per block: the children are few and latency-bound
+      if (!ctx->exact_attr_set) {
+        TS_CUDA(cudaFuncSetAttribute(k_score_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(ExactSmem)));
+        TS_CUDA(cudaFuncSetAttribute(k_children_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(ExactSmem)));
+        ctx->exact_attr_set = true;
+      }
+      k_children_exact_mw<<<n, 128, 0, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
+                                                      ctx->rows.as<double>(), ctx->reps.as<int>(), n, state_rows,
+                                                      ctx->raw.as<double>());
+    } else {
+      k_children_exact<<<(n * 32 + 127) / 128, 128, 0, ctx->stream>>>(
+          lstm_weights(ctx), P->pre_exact.as<double>(), T, s, ctx->rows.as<double>(), ctx->reps.as<int>(), n,
+          state_rows, ctx->raw.as<double>());
+    }
     TS_LAUNCHED();
     k_argmin<<<1, 1024, 0, ctx->stream>>>(ctx->raw.as<double>(), ctx->reps.as<int>(), n,
                                           ctx->target_scale, epsilon, rng, ctx->out.as<double>());
