@@ -1149,7 +1149,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
         P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(),
         ctx->status.as<int>());
     TS_LAUNCHED();
-    k_dedup<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
+    k_dedup<<<1, 512, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
     TS_LAUNCHED();
     if (ctx->hidden == 32) {
       // a few warps per block: the children are few and latency-bound
@@ -1160,7 +1160,8 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
                                      (int)sizeof(ExactSmem)));
         ctx->exact_attr_set = true;
       }
-      k_children_exact_mw<<<n, 128, 0, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
+      k_children_exact_mw<<<n, 128, sizeof(double) * F * (T - s), ctx->stream>>>(
+          lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
                                                       ctx->rows.as<double>(), ctx->reps.as<int>(), n, state_rows,
                                                       ctx->raw.as<double>());
     } else {
