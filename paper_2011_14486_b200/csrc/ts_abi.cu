@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1118,8 +1119,13 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
                           ctx->stream));
   TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
   TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * 4096 + sizeof(Nest)));
-  TS_CUDA(ctx->h_out.reserve(sizeof(double) * 2));
+  TS_CUDA(ctx->h_out.reserve(sizeof(double) * 3));
   uint64_t rng = rng_state ? *rng_state : 0;
+  const bool trace = getenv("TS_GREEDY_TRACE") != nullptr;
+  double t_enum = 0.0, t_wait = 0.0;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
   int64_t vis = 0;
   double best_v = 0.0;
   for (int i = 0; i < T; ++i) {
@@ -1128,7 +1134,9 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
     const Nest* cn = sd.consumer >= 0 ? &nests[sd.consumer] : nullptr;
     cands.clear();
+    const double te0 = trace ? now_us() : 0.0;
     const int64_t cnt = enumerate_candidates(sd, cs, cn, [&](const ts_decision& d) { cands.push_back(d); });
+    if (trace) t_enum += now_us() - te0;
     if (cnt <= 0) return fail(ctx, cnt < 0 ? (int)-cnt : TS_ERR_PIPELINE, "candidate enumeration");
     const int n = (int)cnt;
     if (n > 4096) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
@@ -1175,9 +1183,12 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     TS_LAUNCHED();
     double* ho = ctx->h_out.as<double>();
     TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    int* hst = reinterpret_cast<int*>(ho + 2);
+    TS_CUDA(cudaMemcpyAsync(hst, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    const double tw0 = trace ? now_us() : 0.0;
     TS_CUDA(cudaStreamSynchronize(ctx->stream));
-    int st = 0;
-    TS_CUDA(cudaMemcpy(&st, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (trace) t_wait += now_us() - tw0;
+    const int st = *hst;
     if (st) {
       cudaMemset(ctx->status.p, 0, sizeof(int));
       return fail(ctx, st, std::string("device: ") + status_name(st));
@@ -1195,6 +1206,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     TS_CUDA(cudaMemcpyAsync(state_rows + (int64_t)s * F, ctx->rows.as<double>() + (int64_t)best * F,
                             sizeof(double) * F, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  if (trace) fprintf(stderr, "ts_greedy: T %d, host enumeration %.0f us, waiting on the device %.0f us\n", T, t_enum, t_wait);
   if (rng_state && epsilon > 0.0) *rng_state = rng;
   *visited = vis;
   if (out_best_v) *out_best_v = best_v;

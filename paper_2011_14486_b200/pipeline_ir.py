@@ -79,7 +79,10 @@ class Pipeline:
     _cache: dict = field(default_factory=dict, compare=False, repr=False, hash=False)
 
     def __hash__(self):
-        return hash((self.name, self.buffers, self.stages))
+        h = self._cache.get("hash")
+        if h is None:
+            h = self._cache["hash"] = hash((self.name, self.buffers, self.stages))
+        return h
 
     def stage(self, name):
         for s in self.stages:

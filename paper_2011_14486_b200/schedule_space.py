@@ -230,9 +230,17 @@ _INFO: dict = {}
 
 
 def _info(p) -> _PipelineInfo:
+    # per-object cache first: hashing a Pipeline walks every stage
+    cache = getattr(p, "_cache", None)
+    if isinstance(cache, dict):
+        inf = cache.get("ts_info")
+        if inf is not None:
+            return inf
     inf = _INFO.get(p)
     if inf is None:
         inf = _INFO[p] = _PipelineInfo(p)
+    if isinstance(cache, dict):
+        cache["ts_info"] = inf
     return inf
 
 

@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _lib
 from .errors import PipelineError
-from .schedule_space import (_info, candidate_actions, canonical_key, child_state,
+from .schedule_space import (ScheduleState, _info, candidate_actions, canonical_key, child_state,
                              initial_state)
 from .value_model import MODE_EXACT, predict_states
 
@@ -113,9 +113,9 @@ def greedy_schedule_gpu(p, params, noise: NoiseConfig | None = None,
                                     ctypes.byref(visited), ctypes.byref(best_v)))
     if rng is not None and eps > 0:
         rng.state = st.value
-    s = initial_state(p)
-    for i, rec in enumerate(out):
-        s = child_state(s, inf.decode(i, rec))
+    # the chosen records are exactly the encoding of the decoded decisions
+    s = ScheduleState(p, tuple(inf.decode(i, rec) for i, rec in enumerate(out)))
+    s._cache["ts_records"] = out.tobytes()
     if return_value:
         return s, visited.value, best_v.value
     return s, visited.value
