@@ -216,6 +216,63 @@ __device__ __forceinline__ void load_x(const uint4* init_row, const uint4* acq, 
   x4[3] = __ldg(acq + 1);
 }
 
+// One group of 8 hidden units of one row: gate pre-activations (TMEM,
+// pre-scaled by -log2 e / -2 log2 e) -> c (updated in place), h8, readout.
+// Shared by both tensor-core kernels so their rows are bit-identical.
+__device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c, float* h8, float& acc,
+                                           const float* wout) {
+  float ui[8], uf[8], vg[8], uo[8];
+  tmem_ld8(lane_addr + 0 * 32 + g8 * 8, ui);
+  tmem_ld8(lane_addr + 1 * 32 + g8 * 8, uf);
+  tmem_ld8(lane_addr + 2 * 32 + g8 * 8, vg);
+  tmem_ld8(lane_addr + 3 * 32 + g8 * 8, uo);
+  tmem_wait_ld();
+  // Fused cell algebra.  With t_x = 1 + 2^u_x: sigma = 1/t and
+  // tanh = (1 - 2^v)/(1 + 2^v), so
+  //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
+  //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c)).
+  // Units in pairs share each reciprocal (Montgomery's batch
+  // inversion: 1/a = b/(ab), 1/b = a/(ab)): 5 ex2 + 1 rcp per unit.
+  // The denominators are pre-scaled through the FMA constants (t_i by
+  // 2^-60, 1 + e_o by 2^-40, exact) so the pair products stay inside
+  // [2^-120, 2^120] with the exponents clamped at 40 (sigma >= 2^-40).
+  constexpr float S1 = 8.673617379884035e-19f;  // 2^-60
+  constexpr float S2 = 9.094947017729282e-13f;  // 2^-40
+  constexpr float C2 = -2.0f * LOG2E;
+#pragma unroll
+  for (int u = 0; u < 8; u += 2) {
+    float tig[2], num[2], d1[2], eo[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int uu = u + q, j = g8 * 8 + uu;
+      const float ei = ex2_sel(clamp40(ui[uu]), 0), ef = ex2_sel(clamp40(uf[uu]), 1);
+      const float eg = ex2_sel(clamp40(vg[uu]), 2);
+      eo[q] = ex2_sel(clamp40(uo[uu]), 3);
+      // products by (1 + e) as fused a + a e: t_f is never formed
+      const float ti = fmaf(ei, S1, S1);                 // 2^-60 t_i
+      tig[q] = fmaf(ti, eg, ti);                         // 2^-60 t_i t_g
+      const float gm = fmaf(-eg, S1, S1);                // 2^-60 (1 - e_g)
+      num[q] = fmaf(c[j], tig[q], fmaf(gm, ef, gm));     // 2^-60 (c t_i t_g + (1 - e_g) t_f)
+      d1[q] = fmaf(tig[q], ef, tig[q]);                  // 2^-60 t_f t_i t_g
+    }
+    const float r1 = rcp(d1[0] * d1[1]);
+    c[g8 * 8 + u] = num[0] * (d1[1] * r1);
+    c[g8 * 8 + u + 1] = num[1] * (d1[0] * r1);
+    float ec[2], d2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      ec[q] = ex2_sel(clamp40(C2 * c[g8 * 8 + u + q]), 4);
+      const float to = fmaf(eo[q], S2, S2);             // 2^-40 (1 + e_o)
+      d2[q] = fmaf(to, ec[q], to);                       // 2^-40 (1 + e_o)(1 + e_c)
+    }
+    const float r2 = rcp(d2[0] * d2[1]);
+    h8[u] = fmaf(-ec[0], S2, S2) * (d2[1] * r2);
+    h8[u + 1] = fmaf(-ec[1], S2, S2) * (d2[0] * r2);
+    acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
+    acc = fmaf(h8[u + 1], wout[g8 * 8 + u + 1], acc);
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* B = smem;
@@ -323,57 +380,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
       float* prow = (a.record_prefix && r == 0) ? a.pre + (int64_t)(t + 1) * PRE_STRIDE : nullptr;
 #pragma unroll
       for (int g8 = 0; g8 < 4; ++g8) {
-        float ui[8], uf[8], vg[8], uo[8];
-        tmem_ld8(lane_addr + 0 * 32 + g8 * 8, ui);
-        tmem_ld8(lane_addr + 1 * 32 + g8 * 8, uf);
-        tmem_ld8(lane_addr + 2 * 32 + g8 * 8, vg);
-        tmem_ld8(lane_addr + 3 * 32 + g8 * 8, uo);
-        tmem_wait_ld();
         float h8[8];
-        // Fused cell algebra.  With t_x = 1 + 2^u_x: sigma = 1/t and
-        // tanh = (1 - 2^v)/(1 + 2^v), so
-        //   c' = f c + i g = (c t_i t_g + (1 - e_g) t_f) / (t_f t_i t_g)
-        //   h  = o tanh(c') = (1 - e_c) / ((1 + e_o)(1 + e_c)).
-        // Units in pairs share each reciprocal (Montgomery's batch
-        // inversion: 1/a = b/(ab), 1/b = a/(ab)): 5 ex2 + 1 rcp per unit.
-        // The denominators are pre-scaled through the FMA constants (t_i by
-        // 2^-60, 1 + e_o by 2^-40, exact) so the pair products stay inside
-        // [2^-120, 2^120] with the exponents clamped at 40 (sigma >= 2^-40).
-        constexpr float S1 = 8.673617379884035e-19f;  // 2^-60
-        constexpr float S2 = 9.094947017729282e-13f;  // 2^-40
-        constexpr float C2 = -2.0f * LOG2E;
-#pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-          float tig[2], num[2], d1[2], eo[2];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int uu = u + q, j = g8 * 8 + uu;
-            const float ei = ex2_sel(clamp40(ui[uu]), 0), ef = ex2_sel(clamp40(uf[uu]), 1);
-            const float eg = ex2_sel(clamp40(vg[uu]), 2);
-            eo[q] = ex2_sel(clamp40(uo[uu]), 3);
-            // products by (1 + e) as fused a + a e: t_f is never formed
-            const float ti = fmaf(ei, S1, S1);                 // 2^-60 t_i
-            tig[q] = fmaf(ti, eg, ti);                         // 2^-60 t_i t_g
-            const float gm = fmaf(-eg, S1, S1);                // 2^-60 (1 - e_g)
-            num[q] = fmaf(c[j], tig[q], fmaf(gm, ef, gm));     // 2^-60 (c t_i t_g + (1 - e_g) t_f)
-            d1[q] = fmaf(tig[q], ef, tig[q]);                  // 2^-60 t_f t_i t_g
-          }
-          const float r1 = rcp(d1[0] * d1[1]);
-          c[g8 * 8 + u] = num[0] * (d1[1] * r1);
-          c[g8 * 8 + u + 1] = num[1] * (d1[0] * r1);
-          float ec[2], d2[2];
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            ec[q] = ex2_sel(clamp40(C2 * c[g8 * 8 + u + q]), 4);
-            const float to = fmaf(eo[q], S2, S2);             // 2^-40 (1 + e_o)
-            d2[q] = fmaf(to, ec[q], to);                       // 2^-40 (1 + e_o)(1 + e_c)
-          }
-          const float r2 = rcp(d2[0] * d2[1]);
-          h8[u] = fmaf(-ec[0], S2, S2) * (d2[1] * r2);
-          h8[u + 1] = fmaf(-ec[1], S2, S2) * (d2[0] * r2);
-          acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
-          acc = fmaf(h8[u + 1], wout[g8 * 8 + u + 1], acc);
-        }
+        cell_group(lane_addr, g8, c, h8, acc, wout);
         // the UMMA that read A has completed (mbarrier), so h can go straight in
         put_h8(A, r, g8, h8);
         if (prow) {
