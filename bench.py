@@ -7,14 +7,17 @@ scored with the v0 value function - plus the fused greedy wall times.
 
 One process per GPU (torchrun for N>1, NCCL only for the barrier and the
 max-over-ranks reduction of the timings - scoring shards with no data-path
-collective).  A step scores M states per GPU (default 2^20); states are
-generated on the device by the reference's own random walk (SearchRng per
-state, untimed) and stay resident in HBM; records (~280 MB per GPU) exceed
-the 126 MB L2, so no explicit flush is needed between steps.
+collective).  A step scores M states per GPU (default 12.5M, so that the
+8-GPU run is BASELINE configs[3]'s 1e8-state sweep); states are generated on
+the device by the reference's own random walk (SearchRng per state, untimed)
+and stay resident in HBM; records (~3.5 GB per GPU) exceed the 126 MB L2,
+so no explicit flush is needed between steps.
 
 `value`  = states scored per second over all ranks, device-resident inputs.
-`e2e`    = the same through the C-ABI with HOST buffers (ts_score_states):
-           H2D of the records/offsets and D2H of V inside the timed region.
+`e2e`    = the same through the C-ABI with HOST buffers in the wire format
+           predict_states uses for large batches (16-bit action codes + u8
+           depths, ts_score_states_coded): H2D of the codes/depths and D2H of
+           V inside the timed region.
 `cpu_baseline` = the unmodified reference (oracle/_ref, tensched with its
            Cython kernel) on this host: predict_states on fresh VGG-16 states,
            one process and a pool of all cores.
@@ -49,7 +52,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--states", type=int, default=1 << 20, help="states per GPU per step")
+    ap.add_argument("--states", type=int, default=12_500_000,
+                    help="states per GPU per step (default: 1e8 over 8 GPUs)")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--cpu-states", type=int, default=1500, help="reference states per process")
     ap.add_argument("--no-cpu", action="store_true")
@@ -382,29 +386,21 @@ def main():
     value = total_states / (ms_max / 1e3)
 
     # ---- e2e: host buffers through the C-ABI (pinned), H2D + D2H inside
-    h_recs = torch.empty(n_records * 16, dtype=torch.uint8, pin_memory=True)
-    h_recs.copy_(recs[: n_records * 16])
     h_offs = torch.empty(M + 1, dtype=torch.int64, pin_memory=True)
     h_offs.copy_(offs)
     h_out = torch.empty(M, dtype=torch.float64, pin_memory=True)
-    # the 8-byte wire format (ts_score_states_packed): what predict_states
-    # sends for large batches
     # the wire format predict_states sends for large batches: 16-bit action
-    # codes (ts_score_states_coded) when every decision is in
-    # candidate_actions' space (always, for these walks), else 8-byte packed
-    from paper_2011_14486_b200.schedule_space import action_codes
-    np_recs = np.frombuffer(h_recs.numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
-    codes = action_codes(inf, np_recs, h_offs.numpy())
-    h_depth = torch.from_numpy(np.diff(h_offs.numpy()).astype(np.uint8)).pin_memory()
-    if codes is not None:
-        h_wire = torch.from_numpy(codes.view(np.int16)).pin_memory()
-        wire_name = "16-bit action codes + u8 depths (ts_score_states_coded)"
-        wire_fn = ctx.lib.ts_score_states_coded
-    else:
-        packed = _lib.pack_records(np_recs)
-        h_wire = torch.from_numpy(packed.view(np.int64)).pin_memory()
-        wire_name = "8-byte packed decisions + u8 depths (ts_score_states_packed)"
-        wire_fn = ctx.lib.ts_score_states_packed
+    # codes (ts_score_states_coded), every decision of these walks being in
+    # candidate_actions' space; prepared outside the timed region (encoded
+    # on the device here, as schedule_space.action_codes does on the host)
+    d_codes = torch.empty(max(n_records, 1), dtype=torch.int16, device=dev)
+    ctx.check(ctx.lib.ts_encode_codes_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M, d_codes.data_ptr()))
+    h_wire = torch.empty(n_records, dtype=torch.int16, pin_memory=True)
+    h_wire.copy_(d_codes[:n_records])
+    h_depth = torch.empty(M, dtype=torch.uint8, pin_memory=True)
+    h_depth.copy_((offs[1:] - offs[:-1]).to(torch.uint8))
+    wire_name = "16-bit action codes + u8 depths (ts_score_states_coded)"
+    wire_fn = ctx.lib.ts_score_states_coded
     e2e_h2d = int(h_wire.numel() * h_wire.element_size() + M)
 
     def e2e_step():

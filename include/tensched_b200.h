@@ -142,6 +142,16 @@ int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed,
 int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
                           int64_t n_states, int mode, double* out_v);
 
+/* Records -> action codes on the host (inverse of ts_decode_codes);
+ * TS_ERR_ILLEGAL when a decision lies outside the code space. */
+int ts_encode_codes(ts_ctx* ctx, int pipeline_id, const ts_decision* records, const uint8_t* depths,
+                    int64_t n_states, uint16_t* out_codes);
+
+/* Device-resident records -> action codes (the inverse of the decoding);
+ * TS_ERR_ILLEGAL when a decision lies outside the code space. */
+int ts_encode_codes_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records, const int64_t* d_offsets,
+                           int64_t n_states, uint16_t* d_codes);
+
 /* Decodes action codes to records on the host (state i's decision j belongs
  * to schedule position j); for tests and tools.  Host-only contexts work. */
 int ts_decode_codes(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,

@@ -97,6 +97,8 @@ def load_library():
             "ts_score_states_packed": ([vp, i32, vp, vp, i64, i32, vp], i32),
             "ts_score_states_coded": ([vp, i32, vp, vp, i64, i32, vp], i32),
             "ts_decode_codes": ([vp, i32, vp, vp, i64, vp], i32),
+            "ts_encode_codes_device": ([vp, i32, vp, vp, i64, vp], i32),
+            "ts_encode_codes": ([vp, i32, vp, vp, i64, vp], i32),
             "ts_lstm_forward": ([vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, f64, i32, vp], i32),
             "ts_candidates": ([vp, i32, vp, i64, vp, i64, ctypes.POINTER(i64)], i32),
             "ts_check_action": ([vp, i32, vp, i64, vp], i32),

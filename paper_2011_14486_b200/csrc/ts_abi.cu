@@ -962,6 +962,39 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
   return check_device_status(ctx);
 }
 
+int ts_encode_codes_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records, const int64_t* d_offsets,
+                           int64_t n_states, uint16_t* d_codes) {
+  if (!ctx || !d_offsets || n_states < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  k_encode_codes<<<(unsigned)((n_states + 255) / 256), 256, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, d_codes, ctx->status.as<int>());
+  TS_LAUNCHED();
+  return check_device_status(ctx);
+}
+
+int ts_encode_codes(ts_ctx* ctx, int pipeline_id, const ts_decision* records, const uint8_t* depths,
+                    int64_t n_states, uint16_t* out_codes) {
+  if (!ctx || !depths || n_states < 0) return TS_ERR_ARG;
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  int64_t r = 0;
+  for (int64_t i = 0; i < n_states; ++i) {
+    if (depths[i] > T) return fail(ctx, TS_ERR_ARG, "depth exceeds the pipeline's stages");
+    for (int j = 0; j < depths[i]; ++j, ++r) {
+      const uint32_t c = encode_action(D.st[T - 1 - j], records[r]);
+      if (c > 0xFFFEu) return fail(ctx, TS_ERR_ILLEGAL, "decision outside the action-code space");
+      out_codes[r] = (uint16_t)c;
+    }
+  }
+  return TS_OK;
+}
+
 int ts_decode_codes(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, const uint8_t* depths,
                     int64_t n_states, ts_decision* out_records) {
   if (!ctx || !depths || n_states < 0) return TS_ERR_ARG;

@@ -657,6 +657,41 @@ TS_HD ts_decision decode_action(const StageDesc& s, uint32_t code) {
   return d;
 }
 
+// Inverse of decode_action: the code whose decoding is `d`, or 0xFFFF when
+// `d` lies outside candidate_actions' space.
+TS_HD uint32_t encode_action(const StageDesc& s, const ts_decision& d) {
+  if (d.anchor < -1 || d.anchor > 2 || d.flags > 3 || (d.vec != 1 && d.vec != 8)) return 0xFFFFu;
+  const int np = s.n_pure;
+  const int first = np >= 2 ? np - 2 : 0;
+  uint32_t sc[2] = {0u, 0u};
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t f = d.split[k];
+    const uint32_t code = f == 0 ? 0u : f == 8 ? 1u : f == 32 ? 2u : 3u;
+    if (k == first && k < np) {
+      sc[0] = code;
+    } else if (k == first + 1 && np >= 2) {
+      sc[1] = code;
+    } else if (f != 0) {
+      return 0xFFFFu;
+    }
+  }
+  if (sc[0] == 3u || sc[1] == 3u) return 0xFFFFu;
+  const uint32_t base = (uint32_t)(d.anchor + 1) | (sc[0] << 2) | (sc[1] << 4) | ((d.vec == 8 ? 1u : 0u) << 8) |
+                        ((uint32_t)(d.flags & 1u) << 9) | ((uint32_t)((d.flags >> 1) & 1u) << 10);
+  uint32_t dw[4];
+  memcpy(dw, &d, sizeof dw);
+  // (placement, swap) in _order_options' order; the first variant that
+  // reproduces the record wins (equal orders decode identically)
+  for (uint32_t v = 0; v < 4; ++v) {
+    const uint32_t code = base | ((v >> 1) << 6) | ((v & 1u) << 7);
+    const ts_decision e = decode_action(s, code);
+    uint32_t ew[4];
+    memcpy(ew, &e, sizeof ew);
+    if (ew[0] == dw[0] && ew[1] == dw[1] && ew[2] == dw[2] && ew[3] == dw[3]) return code;
+  }
+  return 0xFFFFu;
+}
+
 // check_action (schedule_space.py:288-347) on an encoded decision: null if
 // legal, else the violated invariant.  Host only.
 inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const Nest* cn,

@@ -236,6 +236,10 @@ def test_coded_wire_format_matches(gpu_ctx, v0):
     h_offs = offs.cpu().numpy()
     codes = ss.action_codes(inf, h_recs, h_offs)
     assert codes is not None
+    d_codes = torch.empty(len(h_recs), dtype=torch.int16, device="cuda")
+    gpu_ctx.check(gpu_ctx.lib.ts_encode_codes_device(gpu_ctx.h, pid, recs.data_ptr(), offs.data_ptr(), n,
+                                                     d_codes.data_ptr()))
+    assert np.array_equal(d_codes.cpu().numpy().view(np.uint16), codes)  # device encoder == host encoder
     depths = np.diff(h_offs).astype(np.uint8)
     for mode in (MODE_EXACT, MODE_FAST):
         a = np.empty(n)

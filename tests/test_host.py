@@ -99,6 +99,10 @@ def test_action_codes_roundtrip_every_candidate(candidates_golden, greedy_golden
             ctx.check(ctx.lib.ts_decode_codes(ctx.h, pid, _lib._p(codes), _lib._p(depths), len(idxs),
                                               _lib._p(out)))
             assert out.tobytes() == recs.tobytes(), key
+            back = np.zeros(len(recs), dtype=np.uint16)  # native encoder == python encoder
+            ctx.check(ctx.lib.ts_encode_codes(ctx.h, pid, _lib._p(recs), _lib._p(depths), len(idxs),
+                                              _lib._p(back)))
+            assert np.array_equal(back, codes), key
 
 
 def test_action_codes_reject_decisions_outside_the_space(greedy_golden):
