@@ -649,7 +649,9 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       TS_LAUNCHED();
       tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor, rowoff);
       TS_LAUNCHED();
-      tc::k_depth_scatter<<<g, 256, 0, ctx->stream>>>(d_offsets, n_states, cursor, perm);
+      const int64_t per_block = (int64_t)tc::SCATTER_THREADS * tc::SCATTER_PER;
+      tc::k_depth_scatter<<<(unsigned)((n_states + per_block - 1) / per_block), tc::SCATTER_THREADS,
+                            sizeof(int) * 2 * (T + 1), ctx->stream>>>(d_offsets, n_states, T, cursor, perm);
       TS_LAUNCHED();
     }
     TS_CUDA(ctx->rows.reserve(sizeof(float) * 8 * (n_records > 0 ? n_records : 1)));

@@ -469,21 +469,36 @@ __global__ void k_depth_scan(const int* __restrict__ hist, int T, int* __restric
   }
 }
 
-// Warp-aggregated scatter: one atomic per (warp, depth) group.
-__global__ void k_depth_scatter(const int64_t* __restrict__ offsets, int64_t n, int* __restrict__ cursor,
-                                int* __restrict__ perm) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool ok = i < n;
-  const int d = ok ? (int)(offsets[i + 1] - offsets[i]) : -1;
-  const unsigned act = __ballot_sync(0xffffffffu, ok);
-  if (!ok) return;
-  const unsigned peers = __match_any_sync(act, d);
-  const int leader = __ffs(peers) - 1;
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(cursor + d, __popc(peers));
-  base = __shfl_sync(peers, base, leader);
-  perm[base + __popc(peers & ((1u << lane) - 1))] = (int)i;
+// Block-aggregated scatter: each block of SCATTER_THREADS x SCATTER_PER
+// states ranks its states per depth in shared memory and reserves one range
+// per (block, depth) with a single global atomic (the order inside a depth
+// bucket is immaterial: every state's score is independent of its tile).
+constexpr int SCATTER_THREADS = 256, SCATTER_PER = 4;
+__global__ void __launch_bounds__(SCATTER_THREADS) k_depth_scatter(const int64_t* __restrict__ offsets, int64_t n,
+                                                                    int T, int* __restrict__ cursor,
+                                                                    int* __restrict__ perm) {
+  extern __shared__ int sc[];  // cnt[T + 1], base[T + 1]
+  int* cnt = sc;
+  int* base = sc + (T + 1);
+  for (int i = threadIdx.x; i <= T; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * SCATTER_THREADS * SCATTER_PER;
+  int dep[SCATTER_PER], rank[SCATTER_PER];
+#pragma unroll
+  for (int k = 0; k < SCATTER_PER; ++k) {
+    const int64_t i = b0 + k * SCATTER_THREADS + threadIdx.x;
+    dep[k] = i < n ? (int)(offsets[i + 1] - offsets[i]) : -1;
+    rank[k] = dep[k] >= 0 ? atomicAdd(cnt + dep[k], 1) : 0;
+  }
+  __syncthreads();
+  for (int dd = threadIdx.x; dd <= T; dd += blockDim.x)
+    if (cnt[dd]) base[dd] = atomicAdd(cursor + dd, cnt[dd]);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < SCATTER_PER; ++k) {
+    const int64_t i = b0 + k * SCATTER_THREADS + threadIdx.x;
+    if (dep[k] >= 0) perm[base[dep[k]] + rank[k]] = (int)i;
+  }
 }
 
 // --------------------------------------------- host: weight image
