@@ -8,6 +8,9 @@
 // LSTM from the shared prefix and reduces the argmin; only the winner's
 // index comes back.  Only the winner is "applied" (hard part 7).
 #include <cuda_runtime.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include <cub/device/device_scan.cuh>
 #include <chrono>
@@ -92,7 +95,8 @@ struct PipelineSlot {
 struct ts_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;       // compute
-  cudaStream_t copy_stream = nullptr;  // host<->device transfers of ts_score_states
+  cudaStream_t copy_stream = nullptr;  // host->device transfers of ts_score_states*
+  cudaStream_t d2h_stream = nullptr;   // device->host results of ts_score_states_coded
   std::string err;
   std::vector<std::unique_ptr<PipelineSlot>> pipes;
   // parameters
@@ -338,6 +342,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess)
     e = cudaMemcpyToSymbol(d_log2_data, ts_log2_data_bits, sizeof(uint64_t) * TS_LOG2_NDATA);
   if (e == cudaSuccess) e = ctx->status.reserve(sizeof(int));
@@ -383,12 +388,14 @@ void ts_ctx_destroy(ts_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+  if (ctx->d2h_stream) cudaStreamSynchronize(ctx->d2h_stream);
   ctx->pipes.clear();
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
-  cudaStream_t s = ctx->stream, c = ctx->copy_stream;
+  cudaStream_t s = ctx->stream, c = ctx->copy_stream, o = ctx->d2h_stream;
   delete ctx;
   if (s) cudaStreamDestroy(s);
   if (c) cudaStreamDestroy(c);
+  if (o) cudaStreamDestroy(o);
 }
 
 int ts_set_timing(ts_ctx* ctx, int on) {
@@ -701,6 +708,14 @@ static uint64_t sum_bytes(const uint8_t* p, int64_t n) {
   const uint64_t M = 0x00FF00FF00FF00FFull;
   uint64_t total = 0;
   int64_t i = 0;
+#ifdef __SSE2__
+  {  // psadbw: eight byte sums per instruction
+    __m128i acc = _mm_setzero_si128();
+    const __m128i z = _mm_setzero_si128();
+    for (; i + 16 <= n; i += 16) acc = _mm_add_epi64(acc, _mm_sad_epu8(_mm_loadu_si128((const __m128i*)(p + i)), z));
+    total += (uint64_t)_mm_cvtsi128_si64(acc) + (uint64_t)_mm_cvtsi128_si64(_mm_unpackhi_epi64(acc, acc));
+  }
+#endif
   while (i + 8 <= n) {
     uint64_t lanes = 0;
     for (int w = 0; w < 128 && i + 8 <= n; ++w, i += 8) {
@@ -893,14 +908,29 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     rc = ensure_fast_prefix(ctx, P);
     if (rc) return rc;
   }
-  // Codes are 1/8 of the record bytes: a first chunk of a quarter of the
-  // states starts the device while the rest is in flight, and the rest runs
-  // as one batch (full-size launches keep their efficiency).
-  int64_t first = n_states >= (1 << 18) ? n_states / 4 : n_states;
+  // Chunks: codes cost ~36 B per state over PCIe against ~2 ns of device
+  // work, so transfers run well ahead of the compute.  A short first chunk
+  // starts the device early; up to 2^20 states the rest goes as one batch,
+  // beyond that in batches of 2^20 (each result block streams back on its
+  // own stream while the next batch computes; only the last one is exposed).
+  int64_t first = n_states >= (1 << 18) ? std::min<int64_t>(n_states / 4, 1 << 18) : n_states;
+  int64_t step = 1 << 20;
+  bool stepped = n_states > (1 << 20);
   if (const char* e = getenv("TS_CODED_CHUNK")) first = std::max<int64_t>(1024, atoll(e));
+  if (const char* e = getenv("TS_CODED_STEP")) {
+    step = std::max<int64_t>(1024, atoll(e));
+    stepped = true;
+  }
   if (first > n_states) first = n_states;
   std::vector<int64_t> st_at = {0, first};
-  if (first < n_states) st_at.push_back(n_states);
+  if (!stepped) {
+    if (first < n_states) st_at.push_back(n_states);
+  } else {
+    for (int64_t s0 = first; s0 < n_states;) {
+      s0 = std::min(n_states, s0 + step);
+      st_at.push_back(s0);
+    }
+  }
   const int64_t n_chunks = (int64_t)st_at.size() - 1;
   std::vector<int64_t> rec_at(n_chunks + 1);
   {
@@ -956,10 +986,15 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, n_rec, mode,
                       ctx->out.as<double>() + s0, d_codes);
     if (rc) return rc;
+    cudaEvent_t done = take_event(ctx);
+    ev.push_back(done);
+    TS_CUDA(cudaEventRecord(done, ctx->stream));
+    TS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
     TS_CUDA(cudaMemcpyAsync(out_v + s0, ctx->out.as<double>() + s0, sizeof(double) * (s1 - s0),
-                            cudaMemcpyDeviceToHost, ctx->stream));
+                            cudaMemcpyDeviceToHost, ctx->d2h_stream));
   }
   TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
   for (auto e : ev) ctx->event_pool.push_back(e);
   return check_device_status(ctx);
 }

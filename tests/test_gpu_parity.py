@@ -245,16 +245,19 @@ def test_coded_wire_format_matches(gpu_ctx, v0):
         a = np.empty(n)
         gpu_ctx.check(gpu_ctx.lib.ts_score_states(gpu_ctx.h, pid, _lib._p(h_recs), _lib._p(h_offs), n, mode,
                                                   _lib._p(a)))
-        for chunk in (None, "50000"):
+        for chunk, step in ((None, None), ("50000", None), ("20000", "45000")):
             if chunk:
                 os.environ["TS_CODED_CHUNK"] = chunk
+            if step:
+                os.environ["TS_CODED_STEP"] = step
             b = np.empty(n)
             try:
                 gpu_ctx.check(gpu_ctx.lib.ts_score_states_coded(gpu_ctx.h, pid, _lib._p(codes), _lib._p(depths),
                                                                 n, mode, _lib._p(b)))
             finally:
                 os.environ.pop("TS_CODED_CHUNK", None)
-            assert np.array_equal(bits(a), bits(b)), (mode, chunk)
+                os.environ.pop("TS_CODED_STEP", None)
+            assert np.array_equal(bits(a), bits(b)), (mode, chunk, step)
     bad = codes.copy()
     bad[5] = 0xF800  # reserved bits set
     b = np.empty(n)
