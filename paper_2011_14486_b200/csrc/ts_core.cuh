@@ -522,32 +522,37 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn
   // per-invocation consumer region: for each consumer dim read by an edge,
   // the product of that dim's loops strictly inside lvl.  Extents are below
   // 2^31 (descriptor-checked) and so are these products (<= full extents).
-  uint32_t rv[2][TS_MAX_PURE];
-#pragma unroll
-  for (int e = 0; e < 2; ++e)
-#pragma unroll
-    for (int k = 0; k < TS_MAX_PURE; ++k) rv[e][k] = 1u;
+  // Consumer dim of every loop strictly inside lvl, a nibble per loop
+  // (0xF: outside the region), and the loop extents; then per edge map
+  // entry that reads a consumer dim (the stage's cdim: the same for every
+  // state at this decision, so these branches are uniform on the device)
+  // the product of that dim's inner extents.
+  uint32_t dims = 0xFFFFFFFFu;
+  uint32_t m[TS_MAX_LOOPS];
+  const int nl = cn.loops();
 #pragma unroll
   for (int j = 0; j < TS_MAX_LOOPS; ++j) {
-    const uint32_t m = (j > lvl && j < cn.loops()) ? cn.ext_at(j) : 1u;
-    const int dim = loop_dim(cn.id_at(j), cs.n_pure);
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int k = 0; k < TS_MAX_PURE; ++k)
-        if (s.cdim[e][k] == dim) rv[e][k] *= m;
+    m[j] = cn.ext_at(j);
+    const uint32_t dj = (uint32_t)loop_dim(cn.id_at(j), cs.n_pure) & 0xFu;
+    if (j > lvl && j < nl) dims = (dims & ~(0xFu << (4 * j))) | (dj << (4 * j));
   }
 #pragma unroll
-  for (int k = 0; k < TS_MAX_PURE; ++k) {
-    int64_t best = -1;
+  for (int k = 0; k < TS_MAX_PURE; ++k) pe[k] = -1;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      if (e >= s.n_cedges) continue;
+  for (int e = 0; e < 2; ++e) {
+    if (e >= s.n_cedges) continue;
+#pragma unroll
+    for (int k = 0; k < TS_MAX_PURE; ++k) {
       const int cd = s.cdim[e][k];
-      const int64_t ext = cd < 0 ? s.cwindow[e][k] : s.cstride[e][k] * ((int64_t)rv[e][k] - 1) + s.cwindow[e][k];
-      best = ext > best ? ext : best;
+      int64_t ext = s.cwindow[e][k];
+      if (cd >= 0) {
+        uint32_t rv = 1u;
+#pragma unroll
+        for (int j = 0; j < TS_MAX_LOOPS; ++j) rv *= ((dims >> (4 * j)) & 0xFu) == (uint32_t)cd ? m[j] : 1u;
+        ext += s.cstride[e][k] * ((int64_t)rv - 1);
+      }
+      pe[k] = ext > pe[k] ? ext : pe[k];
     }
-    pe[k] = best;
   }
   depth = cn.dep() + lvl + 1;
   return ok ? TS_OK : TS_ERR_OVERFLOW;
