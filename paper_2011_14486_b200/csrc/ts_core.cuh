@@ -576,6 +576,8 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, cons
   if (d.n_loops == 0 || d.n_loops > TS_MAX_LOOPS) return TS_ERR_ILLEGAL;
   out.n_loops = d.n_loops;
   bool bad = false;
+  uint32_t split4;  // split factors, a byte per pure dim
+  memcpy(&split4, d.split, 4);
 #pragma unroll
   for (int j = 0; j < TS_MAX_LOOPS; ++j) {
     const uint8_t id = d.order[j];
@@ -587,7 +589,7 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, cons
     int64_t e;
     if (id < 8) {
       const int k = id >> 1;
-      const int64_t f = k == 0 ? d.split[0] : k == 1 ? d.split[1] : k == 2 ? d.split[2] : d.split[3];
+      const int64_t f = (split4 >> (8 * k)) & 0xFFu;
       const int64_t p = sel4(pe, k);
       bad = bad || k >= s.n_pure || (!f && (id & 1));
       // extents < 2^31 (descriptor-checked): 32-bit division
