@@ -505,9 +505,17 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn
   {
     unsigned __int128 p = ((unsigned __int128)cn.inv_w(1) << 64) | cn.inv_w(0);
     bool fit = cn.inv_w(2) == 0 && cn.inv_w(3) == 0;
+    // candidate_actions anchors at levels 0..2 (MAX_COMPUTE_AT_LEVELS); a
+    // deeper level (legal for hand-written schedules) takes the long loop
+    if (lvl < 3) {
 #pragma unroll
-    for (int j = 0; j < TS_MAX_LOOPS; ++j)
-      if (j <= lvl && j < cn.loops()) p = mul128_64(p, cn.ext_at(j), fit);
+      for (int j = 0; j < 3; ++j)
+        if (j <= lvl && j < cn.loops()) p = mul128_64(p, cn.ext_at(j), fit);
+    } else {
+#pragma unroll
+      for (int j = 0; j < TS_MAX_LOOPS; ++j)
+        if (j <= lvl && j < cn.loops()) p = mul128_64(p, cn.ext_at(j), fit);
+    }
     if (fit) {
       inv.w[0] = (uint64_t)p;
       inv.w[1] = (uint64_t)(p >> 64);

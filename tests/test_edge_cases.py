@@ -120,3 +120,34 @@ def test_single_stage_pipeline_greedy(v0_path):
     P = O.Pipe(p)
     want, wv = O.greedy(P, oracle_params(v0_path))
     assert [d.render() for d in s.decisions] == [a.render() for a in want] and visited == wv
+
+
+@pytest.mark.gpu
+def test_deep_compute_at_levels(v0_path):
+    """compute_at below level 2 (legal for hand-written schedules, never
+    proposed by candidate_actions): features bit-exact against the oracle,
+    V on both legs against the oracle's."""
+    from paper_2011_14486_b200.featurizer import featurize_states
+    from paper_2011_14486_b200.value_model import MODE_FAST, load, predict_states
+    text = ("pipeline deep\nbuffer src dims 66x66 elem 4\n"
+            "stage pre dims x:66,y:66 flops 1\n  in src map x*1+1, y*1+1\n"
+            "stage blur dims x:64,y:64 flops 3 output\n  in pre map x*1+3, y*1+3\n")
+    p = pi.parse_pipeline(text)
+    P = O.Pipe(p)
+    blur = ss.LayerSchedule("blur", (("x", 8), ("y", 8)), ("xo", "xi", "yo", "yi"))
+    states = []
+    for lvl in range(4):
+        pre = ss.LayerSchedule("pre", (), ("x", "y"), 1, False, ("blur", lvl))
+        s = ss.apply(ss.initial_state(p), blur)
+        if ss.check_action(s, pre) is None:
+            states.append(ss.apply(s, pre))
+    assert len(states) >= 3 and any(st.decisions[-1].compute_at[1] == 3 for st in states)
+    decs = [[O.as_act(d) for d in st.decisions] for st in states]
+    feats = featurize_states(states)
+    for f, d in zip(feats, decs):
+        assert np.array_equal(bits(f), bits(O.features(P, d)))
+    params = load(v0_path)
+    want = O.values(oracle_params(v0_path), P, decs)
+    np.testing.assert_allclose(predict_states(params, states), want, rtol=1e-12)
+    np.testing.assert_allclose(predict_states(params, states * 2000, mode=MODE_FAST), np.tile(want, 2000),
+                               rtol=1e-4)
