@@ -1,0 +1,84 @@
+"""Parity on seeded random pipelines (tests/random_pipelines.py) beyond the
+checked-in networks: candidate enumeration (native host enumerator vs the
+oracle, and the oracle vs the built reference when oracle/_ref is present),
+device features, both V legs and the fused greedy vs the oracle."""
+
+import pathlib
+import sys
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import bits
+from random_pipelines import random_pipeline_text
+from paper_2011_14486_b200 import pipeline_ir as pi
+from paper_2011_14486_b200 import schedule_space as ss
+
+SEEDS = range(40)
+REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
+
+
+def _walks(P, n, seed0):
+    return [O.random_partial(P, seed0 + k) for k in range(n)]
+
+
+def test_random_pipeline_candidates_native_vs_oracle():
+    for seed in SEEDS:
+        p = pi.parse_pipeline(random_pipeline_text(seed))
+        P = O.Pipe(p)
+        for decs in _walks(P, 4, 100 * seed + 1):
+            s = ss.initial_state(p)
+            for k in range(len(decs)):
+                want = [a.render() for a in O.candidates(P, decs[:k])]
+                got = [a.render() for a in ss.candidate_actions(s)]
+                assert got == want, (seed, k)
+                s = ss.apply(s, ss.parse_layer_schedule(decs[k].render()))
+
+
+def test_random_pipeline_oracle_vs_reference():
+    """The oracle against the unmodified reference on the same random
+    pipelines (candidates and feature matrices, bit for bit)."""
+    if not (REF / "tensched").exists():
+        pytest.skip("oracle/_ref (the built reference) is not present")
+    sys.path.insert(0, str(REF))
+    from tensched.featurizer import featurize_state
+    from tensched.pipeline_ir import parse_pipeline as ref_parse
+    from tensched.schedule_space import apply as ref_apply
+    from tensched.schedule_space import candidate_actions as ref_candidates
+    from tensched.schedule_space import initial_state as ref_initial
+    for seed in SEEDS:
+        text = random_pipeline_text(seed)
+        P = O.Pipe(pi.parse_pipeline(text))
+        rp = ref_parse(text)
+        for decs in _walks(P, 3, 100 * seed + 7):
+            s = ref_initial(rp)
+            for k in range(len(decs)):
+                cands = ref_candidates(s)
+                assert [a.render() for a in cands] == [a.render() for a in O.candidates(P, decs[:k])], (seed, k)
+                s = ref_apply(s, next(a for a in cands if a.render() == decs[k].render()))
+            assert np.array_equal(bits(np.asarray(featurize_state(s))), bits(O.features(P, decs))), seed
+
+
+@pytest.mark.gpu
+def test_random_pipeline_device_parity(v0_path):
+    from paper_2011_14486_b200.featurizer import featurize_states
+    from paper_2011_14486_b200.search import greedy_schedule_gpu
+    from paper_2011_14486_b200.value_model import MODE_FAST, load, predict_states
+    params = load(v0_path)
+    oparams = O.load_checkpoint(v0_path)
+    for seed in SEEDS:
+        p = pi.parse_pipeline(random_pipeline_text(seed))
+        P = O.Pipe(p)
+        decs = _walks(P, 24, 100 * seed + 3)
+        states = [ss.state_from_decisions(p, d) for d in decs]
+        for f, d in zip(featurize_states(states), decs):
+            assert np.array_equal(bits(f), bits(O.features(P, d))), seed
+        want = O.values(oparams, P, decs)
+        np.testing.assert_allclose(predict_states(params, states), want, rtol=1e-12)
+        reps = -(-4096 // len(states))  # large enough for the compact wire formats
+        np.testing.assert_allclose(predict_states(params, states * reps, mode=MODE_FAST), np.tile(want, reps),
+                                   rtol=1e-4)
+        s, visited = greedy_schedule_gpu(p, params)
+        gw, gv = O.greedy(P, oparams)
+        assert [d.render() for d in s.decisions] == [a.render() for a in gw] and visited == gv, seed
