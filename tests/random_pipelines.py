@@ -10,21 +10,28 @@ import random
 _DIMS = "xyzw"
 
 
-def random_pipeline_text(seed: int) -> str:
+def random_pipeline_text(seed: int, big: bool = False) -> str:
+    """big: 6-12 stages, output extents up to 4096 and longer reductions, so
+    anchor chains reach invocation counts past 2^64."""
     rng = random.Random(seed)
-    n = rng.randint(2, 6)
+    n = rng.randint(6, 12) if big else rng.randint(2, 6)
     names = [f"s{i}" for i in range(n)]
     # stage shapes (extents of non-output stages are filled in later)
     pure = {nm: [(d, None) for d in _DIMS[: rng.randint(1, 3)]] for nm in names}
-    red = {nm: [(f"r{k}", rng.choice([2, 3, 4])) for k in range(rng.choice([0, 0, 1, 2]))] for nm in names}
+    rexts = [3, 5, 7, 16] if big else [2, 3, 4]
+    red = {nm: [(f"r{k}", rng.choice(rexts)) for k in range(rng.choice([0, 0, 1, 2]))] for nm in names}
     out = names[-1]
-    pure[out] = [(d, rng.choice([8, 16, 32, 64])) for d, _ in pure[out]]
+    oexts = [64, 256, 1024, 4096] if big else [8, 16, 32, 64]
+    pure[out] = [(d, rng.choice(oexts)) for d, _ in pure[out]]
     # inputs: every stage reads one or two earlier stages and maybe a buffer;
     # every stage but the output is read by some later stage
     inputs = {nm: [] for nm in names}
     for i in range(1, n):
-        k = rng.randint(1, min(2, i))
-        inputs[names[i]] = rng.sample(names[:i], k)
+        if big:  # a chain (plus a skip edge now and then): long anchor chains
+            inputs[names[i]] = [names[i - 1]] + ([names[i - 2]] if i >= 2 and rng.random() < 0.2 else [])
+        else:
+            k = rng.randint(1, min(2, i))
+            inputs[names[i]] = rng.sample(names[:i], k)
     for j in range(n - 1):
         if not any(names[j] in inputs[names[i]] for i in range(j + 1, n)):
             inputs[names[rng.randint(j + 1, n - 1)]].append(names[j])
@@ -59,7 +66,7 @@ def random_pipeline_text(seed: int) -> str:
             maps.setdefault(nm, []).append((src, clauses))
             prev = need.get(src, [0] * arity)
             need[src] = [max(a, b) for a, b in zip(prev, foot)]
-    lines = [f"pipeline rp{seed}"]
+    lines = [f"pipeline rp{'big' if big else ''}{seed}"]
     for b, ar in buffers:
         ext = need.get(b, [1] * ar)
         lines.append(f"buffer {b} dims {'x'.join(str(max(e, 1)) for e in ext)} elem {rng.choice([1, 2, 4])}")

@@ -16,6 +16,11 @@ from paper_2011_14486_b200 import pipeline_ir as pi
 from paper_2011_14486_b200 import schedule_space as ss
 
 SEEDS = range(40)
+BIG = range(1000, 1012)  # random_pipeline_text(seed, big=True)
+
+
+def _texts():
+    return [random_pipeline_text(s) for s in SEEDS] + [random_pipeline_text(s, big=True) for s in BIG]
 REF = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
 
 
@@ -24,8 +29,8 @@ def _walks(P, n, seed0):
 
 
 def test_random_pipeline_candidates_native_vs_oracle():
-    for seed in SEEDS:
-        p = pi.parse_pipeline(random_pipeline_text(seed))
+    for seed, text in enumerate(_texts()):
+        p = pi.parse_pipeline(text)
         P = O.Pipe(p)
         for decs in _walks(P, 4, 100 * seed + 1):
             s = ss.initial_state(p)
@@ -47,8 +52,7 @@ def test_random_pipeline_oracle_vs_reference():
     from tensched.schedule_space import apply as ref_apply
     from tensched.schedule_space import candidate_actions as ref_candidates
     from tensched.schedule_space import initial_state as ref_initial
-    for seed in SEEDS:
-        text = random_pipeline_text(seed)
+    for seed, text in enumerate(_texts()):
         P = O.Pipe(pi.parse_pipeline(text))
         rp = ref_parse(text)
         for decs in _walks(P, 3, 100 * seed + 7):
@@ -67,8 +71,8 @@ def test_random_pipeline_device_parity(v0_path):
     from paper_2011_14486_b200.value_model import MODE_FAST, load, predict_states
     params = load(v0_path)
     oparams = O.load_checkpoint(v0_path)
-    for seed in SEEDS:
-        p = pi.parse_pipeline(random_pipeline_text(seed))
+    for seed, text in enumerate(_texts()):
+        p = pi.parse_pipeline(text)
         P = O.Pipe(p)
         decs = _walks(P, 24, 100 * seed + 3)
         states = [ss.state_from_decisions(p, d) for d in decs]
