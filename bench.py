@@ -56,6 +56,8 @@ def parse_args():
                     help="states per GPU per step (default: 1e8 over 8 GPUs)")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--cpu-states", type=int, default=1500, help="reference states per process")
+    ap.add_argument("--cpu-repeats", type=int, default=10,
+                    help="scoring passes over fresh copies of the reference states (~8 s of timed CPU work)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-greedy", action="store_true")
     ap.add_argument("--no-train", action="store_true")
@@ -143,7 +145,8 @@ def _ref_import():
 def _ref_worker(args):
     """Generate n fresh states with the reference's own walk (untimed), then
     time the reference's predict_states on them (features not cached)."""
-    seed0, n, ckpt = args
+    seed0, n, ckpt = args[:3]
+    repeats = args[3] if len(args) > 3 else 1
     _ref_import()
     from tensched.pipeline_ir import parse_pipeline
     from tensched.schedule_space import apply, candidate_actions, initial_state
@@ -151,21 +154,35 @@ def _ref_worker(args):
     from tensched.value_model import load, predict_states
     params = load(ckpt)
     p = parse_pipeline(VGG.read_text())
-    states = []
+    walks = []
     for seed in range(seed0, seed0 + n):
         rng = SearchRng(seed)
         d = rng.randrange(len(p.stages)) + 1
         s = initial_state(p)
+        acts = []
         for _ in range(d):
             c = candidate_actions(s)
-            s = apply(s, c[rng.randrange(len(c))])
-        states.append(s)
-    t0 = time.perf_counter()
-    predict_states(params, states, jobs=1)
-    return time.perf_counter() - t0, len(states)
+            acts.append(c[rng.randrange(len(c))])
+            s = apply(s, acts[-1])
+        walks.append(acts)
+    # `repeats` passes, each over FRESH state objects rebuilt from the walks'
+    # actions (untimed), so no pass reuses the features the reference caches
+    # on a state (featurizer.py:72-73)
+    dt = 0.0
+    for _ in range(repeats):
+        states = []
+        for acts in walks:
+            s = initial_state(p)
+            for a in acts:
+                s = apply(s, a)
+            states.append(s)
+        t0 = time.perf_counter()
+        predict_states(params, states, jobs=1)
+        dt += time.perf_counter() - t0
+    return dt, n * repeats
 
 
-def cpu_reference(per_proc: int, seed0: int = 1, single: bool = True):
+def cpu_reference(per_proc: int, seed0: int = 1, single: bool = True, repeats: int = 1):
     """The reference's own predict_states on fresh VGG-16 sweep states: one
     process, then a pool of os.cpu_count() processes over disjoint shards."""
     import multiprocessing as mp
@@ -173,14 +190,14 @@ def cpu_reference(per_proc: int, seed0: int = 1, single: bool = True):
     ckpt = str(GOLD / "v0.ckpt")
     out = {}
     if single:
-        dt, n = _ref_worker((seed0, per_proc, ckpt))
+        dt, n = _ref_worker((seed0, per_proc, ckpt, repeats))
         out["single"], out["single_sample"] = n / dt, n
     cores = os.cpu_count() or 1
-    shards = [(seed0 + i * per_proc, per_proc, ckpt) for i in range(cores)]
+    shards = [(seed0 + i * per_proc, per_proc, ckpt, repeats) for i in range(cores)]
     with mp.get_context("spawn").Pool(cores) as pool:
         res = pool.map(_ref_worker, shards)
     out["pool"] = sum(r[1] for r in res) / max(r[0] for r in res)
-    out["pool_sample"] = per_proc * cores
+    out["pool_sample"] = per_proc * cores * repeats
     out["cores"] = cores
     return out
 
@@ -479,12 +496,14 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
-            r = cpu_reference(args.cpu_states)
+            r = cpu_reference(args.cpu_states, repeats=args.cpu_repeats)
             cpu = {"value": r["pool"], "unit": "states/s", "cores": r["cores"], "kind": "reference",
                    "single_process": r["single"],
                    "sample": f"tensched predict_states (Cython) on fresh VGG-16 sweep states: "
                              f"{r['single_sample']} states in 1 process, {r['pool_sample']} over "
-                             f"{r['cores']} processes"}
+                             f"{r['cores']} processes ({args.cpu_states} walks per process, "
+                             f"scored {args.cpu_repeats}x as fresh state objects, so features are "
+                             f"recomputed every pass)"}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "states/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
