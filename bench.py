@@ -296,27 +296,44 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
             torch.cuda.synchronize(dev)
         g.apply(1e-3, 5.0, gbuf.data_ptr())
 
-    for _ in range(3):
-        step()
-    g.sync()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K = max(5, args.steps * 2)
-    e0.record(stream)
-    for _ in range(K):
-        step()
-    e1.record(stream)
-    g.sync()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    final = g.get_params()
-    assert np.all(np.isfinite(final))
-    return {"metric": "V-training samples/sec", "value": B * world * K / (ms / 1e3),
+    p0 = flat_params(params)
+
+    def timed(mode):
+        g.set_mode(mode)
+        g.set_params(p0)
+        for _ in range(3):
+            step()
+        g.sync()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            step()
+        e1.record(stream)
+        g.sync()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        final = g.get_params()
+        assert np.all(np.isfinite(final))
+        return float(ms.item())
+
+    ms_exact = timed("exact")
+    ms_tc = timed("tc")
+    g.set_mode("exact")
+    # algorithmic weight-gradient flops of one step: 2 * 128 x 49 ([x | h_prev | 1])
+    # per (sequence, timestep) pair; every sample of this dataset has T timesteps
+    wg_flops = 2.0 * 128 * 49 * T * B
+    return {"metric": "V-training samples/sec", "value": B * world * K / (ms_tc / 1e3),
             "unit": "samples/s", "pairs_per_gpu": N, "schedules_per_gpu": S, "batch_per_gpu": B,
-            "global_batch": B * world, "steps": K, "ms_per_step": ms / K, "dtype": "f64",
+            "global_batch": B * world, "steps": K, "ms_per_step": ms_tc / K,
+            "mode": "tc: fp64 forward/BPTT, weight gradients on tcgen05 (3xTF32, TMEM, fused into BPTT)",
+            "dtype": "f64 recurrences + tf32x3 weight-gradient GEMM",
+            "weight_grad_tflops_per_step": wg_flops / 1e12,
+            "exact": {"value": B * world * K / (ms_exact / 1e3), "ms_per_step": ms_exact / K,
+                      "dtype": "f64", "note": "fp64 throughout: the reference's trajectory"},
             "parallelism": f"dp{world}", "collective": "NCCL all_reduce(sum) of the gradient"
                                                        if world > 1 else "none",
             "targets": "device cost oracle (cost_oracle.benchmark) of each prefix's schedule"}

@@ -235,6 +235,14 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
                    double* d_grad, double* raw_out);
 /* _clip (global L2 incl. b_out) + SGD with the gradient in d_grad. */
 int ts_train_apply(ts_ctx* ctx, const double* d_grad, double lr, double clip_norm, double* norm_out);
+/* Gradient arithmetic of ts_train_grads.  TS_TRAIN_EXACT (default): fp64
+ * throughout, the reference's trajectory (value_model.gradients,
+ * value_model.py:182-210).  TS_TRAIN_TC: fp64 forward/BPTT recurrences with
+ * the weight-gradient contraction on the tensor cores (3xTF32, fp32
+ * accumulation in TMEM, fused into BPTT; hidden size 32 only). */
+#define TS_TRAIN_EXACT 0
+#define TS_TRAIN_TC 1
+int ts_train_set_mode(ts_ctx* ctx, int mode);
 /* raw scores of dataset entries idx[0..n) (for _eval_split). */
 int ts_train_forward(ts_ctx* ctx, const int32_t* idx, int64_t n, double* raw_out);
 

@@ -112,6 +112,7 @@ struct ts_ctx {
   int sm_count = 148;
   bool tc_attr_set = false;
   bool exact_attr_set = false;
+  bool tr_tc_attr_set = false;
   // optional per-kernel-class timing (bench.py): events around launches on
   // the context stream, resolved at the next host synchronization
   bool timing = false;
@@ -125,6 +126,7 @@ struct ts_ctx {
   int64_t kcount[TS_KCLASSES] = {0};
   // V training (ts_train_*)
   int tr_H = 0, tr_Tmax = 0;
+  int tr_mode = TS_TRAIN_EXACT;
   int64_t tr_N = 0;
   DevBuf tr_X, tr_T, tr_logt, tr_P, tr_grad, tr_cache, tr_dz, tr_raw, tr_draw, tr_batch, tr_norm, tr_partial,
       tr_pvalid;
@@ -1499,6 +1501,13 @@ static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs&
   a.H = ctx->tr_H;
   a.target_scale = 0.0;
   a.n_total = 1.0;
+  a.partial = nullptr;
+  return TS_OK;
+}
+
+int ts_train_set_mode(ts_ctx* ctx, int mode) {
+  if (!ctx || (mode != TS_TRAIN_EXACT && mode != TS_TRAIN_TC)) return TS_ERR_ARG;
+  ctx->tr_mode = mode;
   return TS_OK;
 }
 
@@ -1522,6 +1531,31 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
   if (rc) return rc;
   const bool grouped = ctx->tr_H == tr::GH && !getenv("TS_TRAIN_WARP");
   const int64_t K = (int64_t)ctx->tr_Tmax * B;
+  if (ctx->tr_mode == TS_TRAIN_TC) {
+    // fp64 recurrences, weight gradients on the tensor cores fused into BPTT
+    if (ctx->tr_H != tr::GH) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
+    TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
+    a.cache = ctx->tr_cache.as<double>();
+    a.target_scale = target_scale;
+    a.n_total = (double)n_total;
+    const int nblk = (int)((B + tr::GS - 1) / tr::GS);
+    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * nblk * L.n));
+    a.partial = ctx->tr_partial.as<double>();
+    if (!ctx->tr_tc_attr_set) {
+      TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(tr::GroupSmem)));
+      ctx->tr_tc_attr_set = true;
+    }
+    tr::k_train_fb_group<true><<<nblk, tr::GTHREADS, sizeof(tr::GroupSmem), ctx->stream>>>(a);
+    TS_LAUNCHED();
+    tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), nblk, L.n, grad);
+    TS_LAUNCHED();
+    if (raw_out) {
+      TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
+      TS_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return TS_OK;
+  }
   TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
   TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * K * (grouped ? tr::PROW : L.G)));
   a.cache = ctx->tr_cache.as<double>();
@@ -1535,9 +1569,9 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
     a.pvalid = ctx->tr_pvalid.as<uint8_t>();
     // grouped kernels (bit-identical forward/BPTT; weight gradients in the
     // same pair order within each of ksplit ranges)
-    TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(tr::GroupSmem)));
-    tr::k_train_fb_group<<<(unsigned)((B + tr::GS - 1) / tr::GS), tr::GTHREADS, sizeof(tr::GroupSmem),
+    tr::k_train_fb_group<false><<<(unsigned)((B + tr::GS - 1) / tr::GS), tr::GTHREADS, sizeof(tr::GroupSmem),
                            ctx->stream>>>(a);
     TS_LAUNCHED();
     ksplit = (int)std::min<int64_t>(2 * ctx->sm_count, std::max<int64_t>(1, K / 64));

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include "ts_core.cuh"
+#include "ts_lstm_tc.cuh"
 
 namespace ts {
 namespace tr {
@@ -73,6 +74,7 @@ struct TrainArgs {
   int B, Tmax, H;
   double target_scale;
   double n_total;       // global minibatch size n (value_model.py:193)
+  double* partial;      // tensor-core weight gradients: [gridDim.x][n_params] per-CTA sums
 };
 
 __global__ void k_train_fb(TrainArgs a) {
@@ -290,8 +292,64 @@ struct GroupSmem {
   const double* xinit[GS];  // per sequence: init rows (t < T - d)
   const double* xrows[GS];  //               scheduled rows, reversed (t >= T - d)
   int T[GS], Tu[GS];        // length, first scheduled timestep T - d
+  uint64_t bar[2];          // tensor-core weight gradients: UMMA completion per operand buffer
+  uint32_t tmem;            //                               TMEM accumulator base
 };
 
+// ------------------------------------------------ tensor-core weight gradients
+// kTc = true (ts_train_set_mode(TS_TRAIN_TC)): the forward and BPTT
+// recurrences stay fp64 (raw, d_raw and every dz are the exact kernel's), but
+// the weight-gradient contraction - the one dense GEMM of training,
+// [dWx; dWh; db]^T = sum over (sequence, timestep) of dz^T [x | h_prev | 1],
+// K = B * T - runs on the tensor cores, fused into BPTT: at every timestep
+// the CTA's 16 dz rows (A = dz^T, M = 128 gate columns, K = 16 sequences)
+// and [x_t | h_{t-1} | 1] rows (B, N = 64) are split into TF32 hi/lo in
+// shared memory (the forward weight tile's space, free during BPTT) and one
+// thread issues six kind::tf32 UMMAs, A' = [hi | lo | hi] . B' = [hi | hi |
+// lo] (3xTF32, ~22-bit operands), accumulating D[128 x 64] (fp32) in TMEM
+// over the CTA's whole BPTT.  No pair rows go to HBM and the separate
+// weight-gradient kernel disappears; the CTA writes its D (and the fp64 dw,
+// db_out sums) as one partial, reduced in fixed order by k_train_reduce.
+constexpr int TCN = 64;                          // UMMA N: x(16) | h_prev(32) | 1 | 0 x 15
+constexpr int TC_CS_A = (GG / 8) * 128;          // A: bytes between K chunks = 2048
+constexpr int TC_CS_B = (TCN / 8) * 128;         // B: 1024
+constexpr int TC_A_BYTES = (GS / 4) * TC_CS_A;   // one K = 16 operand: 8192
+constexpr int TC_B_BYTES = (GS / 4) * TC_CS_B;   // 4096
+constexpr int TC_BUF = 2 * TC_A_BYTES + 2 * TC_B_BYTES;  // A_hi, A_lo, B_hi, B_lo = 24576
+static_assert(2 * TC_BUF <= (int)sizeof(double) * GK * GG, "two operand buffers fit the W tile");
+// kind::tf32, A = B = TF32, D = F32, K-major both, N = 64, M = 128
+constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TCN >> 3) << 17) |
+                              ((uint32_t)(GG >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(TC_IDESC), "r"(acc)
+      : "memory");
+}
+
+// round to the nearest TF32 (ties away from zero) on the integer pipe - the
+// bit pattern of cvt.rna.tf32.f32 for finite values, without the conversion
+// unit; the tensor core reads the top 19 bits
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+}
+
+// v = hi + lo + O(2^-22 |v|), both TF32 (fp32 bit patterns, low 13 bits 0);
+// one f64 -> f32 conversion, the remainder f - hi is exact in fp32
+__device__ __forceinline__ void split_tf32(double v, uint32_t& hi, uint32_t& lo) {
+  const float f = (float)v;
+  hi = tf32_rna(f);
+  lo = tf32_rna(__fsub_rn(f, __uint_as_float(hi)));
+}
+
+// canonical K-major no-swizzle offset of element (row, k), 4-byte elements
+__device__ __forceinline__ int tc_off(int row, int k, int cs) {
+  return (k >> 2) * cs + (row >> 3) * 128 + (row & 7) * 16 + (k & 3) * 4;
+}
+
+template <bool kTc>
 __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
   extern __shared__ __align__(16) double tr_dyn_smem[];
   GroupSmem& S = *reinterpret_cast<GroupSmem*>(tr_dyn_smem);
@@ -320,7 +378,23 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
     S.xinit[tid] = xi;
     S.xrows[tid] = xr;
   }
+  if constexpr (kTc) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       tc::smem_u32(&S.tmem)),
+                   "r"(TCN)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+      tc::mbar_init(&S.bar[0], 1);
+      tc::mbar_init(&S.bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_before();
+  }
   __syncthreads();
+  if constexpr (kTc) tc::fence_after();
   int Tg = 0;
   for (int s = 0; s < GS; ++s) Tg = max(Tg, S.T[s]);
   // gate-phase ownership: sequence s = warp + 8q, hidden unit j = lane
@@ -341,7 +415,7 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       double v = 0.0;
       if (t < S.T[s]) {
         v = t < S.Tu[s] ? S.xinit[s][t * F + k] : S.xrows[s][k - t * F];
-        a.dz[((int64_t)(a.Tmax - 1 - t) * a.B + g0 + s) * PROW + k] = v;
+        if constexpr (!kTc) a.dz[((int64_t)(a.Tmax - 1 - t) * a.B + g0 + s) * PROW + k] = v;
       }
       S.xh[s][k] = v;
     }
@@ -383,11 +457,15 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       cc[3 * GH + lane] = go;
       cc[4 * GH + lane] = c_prev;
       cc[6 * GH + lane] = tc;
-      const int64_t kk = (int64_t)(a.Tmax - 1 - t) * a.B + g0 + s;
-      double* pr = a.dz + kk * PROW;
-      pr[16 + lane] = h_prev;
-      pr[48 + lane] = h;
-      if (lane == 0) a.pvalid[kk] = 1;
+      if constexpr (kTc) {
+        cc[7 * GH + lane] = h;  // h_prev of t + 1 as well
+      } else {
+        const int64_t kk = (int64_t)(a.Tmax - 1 - t) * a.B + g0 + s;
+        double* pr = a.dz + kk * PROW;
+        pr[16 + lane] = h_prev;
+        pr[48 + lane] = h;
+        if (lane == 0) a.pvalid[kk] = 1;
+      }
       hn[q] = h;
       const double prod = fmul(h, S.w[lane]);
       double acc = 0.0;
@@ -416,7 +494,8 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
   // into registers while the current dh_next product runs
   double dh_next[2] = {0.0, 0.0}, dc_next[2] = {0.0, 0.0};
   const double wj = S.w[lane];
-  double cv[2][6];
+  constexpr int NCV = kTc ? 8 : 6;
+  double cv[2][NCV];
   auto load_cache = [&](int t) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -428,14 +507,45 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       cv[q][3] = cc[3 * GH];
       cv[q][4] = cc[4 * GH];
       cv[q][5] = cc[6 * GH];
+      if constexpr (kTc) {
+        // h_t (dw) and h_{t-1} (the B operand): h_t is the previous call's
+        // h_{t-1} except at a sequence's last timestep
+        cv[q][7] = t == Tq[q] - 1 ? cc[7 * GH] : cv[q][6];
+        cv[q][6] = t > 0 ? cc[7 * GH - CACHE_FIELDS * GH] : 0.0;
+      }
     }
   };
+  // tensor-core operands, two buffers in the (now unused) forward weight
+  // tile, each [A_hi | A_lo | B_hi | B_lo] (K = 16 sequences); the UMMAs of
+  // timestep t read buffer t & 1 while the next timestep fills the other
+  uint8_t* tcbuf = reinterpret_cast<uint8_t*>(&S.W[0][0]);
+  // per buffer (bit bf): phase parity and a commit in flight - at most one
+  // per barrier, so a parity wait never skips a phase
+  uint32_t phase = 0u, pending = 0u;
+  int n_issued = 0;  // uniform: UMMA groups issued (TMEM holds a partial sum once > 0)
+  double dw_acc[2] = {0.0, 0.0};
+  if constexpr (kTc) {
+    // B rows 49..63 stay zero in both buffers (row 48 is the ones column of db)
+    for (int e = tid; e < 2 * 2 * 15 * 4; e += GTHREADS) {
+      const int buf = e / 120, half = (e / 60) & 1, row = 49 + (e % 60) / 4, c4 = e % 4;
+      *reinterpret_cast<uint4*>(tcbuf + buf * TC_BUF + 2 * TC_A_BYTES + half * TC_B_BYTES +
+                                tc_off(row, 4 * c4, TC_CS_B)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
   load_cache(Tg - 1);
   for (int t = Tg - 1; t >= 0; --t) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      if (t >= Tq[q]) continue;
       const int s = warp + 8 * q, b = g0 + s;
+      if (t >= Tq[q]) {
+        if constexpr (kTc) {  // this sequence adds nothing at t: zero operand rows
+#pragma unroll
+          for (int g = 0; g < 4; ++g) S.zb[s][g * GH + lane] = 0.0;
+          S.xh[s][16 + lane] = 0.0;
+          if (lane < 16) S.xh[s][lane] = 0.0;
+        }
+        continue;
+      }
       const double gi = cv[q][0], gf = cv[q][1], gg = cv[q][2], go = cv[q][3];
       const double c_prev = cv[q][4], tc = cv[q][5];
       const double dh = fadd(fmul(wj, d_raw[q]), dh_next[q]);
@@ -447,11 +557,19 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       const double dzf = fmul(fmul(df, gf), fsub(1.0, gf));
       const double dzg = fmul(dg, fsub(1.0, fmul(gg, gg)));
       const double dzo = fmul(fmul(d_o, go), fsub(1.0, go));
-      double* dzt = a.dz + ((int64_t)(a.Tmax - 1 - t) * a.B + b) * PROW + 80;
-      dzt[lane] = dzi;
-      dzt[GH + lane] = dzf;
-      dzt[2 * GH + lane] = dzg;
-      dzt[3 * GH + lane] = dzo;
+      if constexpr (kTc) {
+        (void)b;
+        // [x_t | h_{t-1}] of this sequence for the B operand
+        S.xh[s][16 + lane] = cv[q][6];
+        if (lane < 16) S.xh[s][lane] = t < S.Tu[s] ? S.xinit[s][t * F + lane] : S.xrows[s][lane - t * F];
+        dw_acc[q] = ffma(cv[q][7], d_raw[q], dw_acc[q]);  // dw = sum_t h_t d_raw
+      } else {
+        double* dzt = a.dz + ((int64_t)(a.Tmax - 1 - t) * a.B + b) * PROW + 80;
+        dzt[lane] = dzi;
+        dzt[GH + lane] = dzf;
+        dzt[2 * GH + lane] = dzg;
+        dzt[3 * GH + lane] = dzo;
+      }
       S.zb[s][lane] = dzi;
       S.zb[s][GH + lane] = dzf;
       S.zb[s][2 * GH + lane] = dzg;
@@ -459,6 +577,39 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
     }
     load_cache(t - 1);
     __syncthreads();
+    if constexpr (kTc) {
+      // operand tiles from S.zb / S.xh, one 16-byte chunk (4 sequences) per
+      // item and segment, consecutive threads on consecutive rows (conflict
+      // free); first the previous timestep's UMMAs must have read the tiles
+      // buffer t & 1 was last read by the UMMAs of timestep t + 2: wait for
+      // that commit (on the buffer's own barrier)
+      const int bf = t & 1;
+      if ((pending >> bf) & 1u) {
+        tc::mbar_wait(&S.bar[bf], (phase >> bf) & 1u);
+        phase ^= 1u << bf;
+        pending &= ~(1u << bf);
+      }
+      uint8_t* At = tcbuf + (t & 1) * TC_BUF;
+      uint8_t* Bt = At + 2 * TC_A_BYTES;
+      for (int e = tid; e < GG * 4 + 49 * 4; e += GTHREADS) {
+        const bool isa = e < GG * 4;
+        const int e2 = isa ? e : e - GG * 4;
+        const int row = isa ? (e2 & (GG - 1)) : e2 % 49, c4 = isa ? (e2 >> 7) : e2 / 49;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int sq = 4 * c4 + u;
+          const double v = isa ? S.zb[sq][row] : (row < 48 ? S.xh[sq][row] : (t < S.T[sq] ? 1.0 : 0.0));
+          split_tf32(v, hi[u], lo[u]);
+        }
+        const uint4 H4 = make_uint4(hi[0], hi[1], hi[2], hi[3]), L4 = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        uint8_t* dst = isa ? At + tc_off(row, 4 * c4, TC_CS_A) : Bt + tc_off(row, 4 * c4, TC_CS_B);
+        const int lo_off = isa ? TC_A_BYTES : TC_B_BYTES;
+        *reinterpret_cast<uint4*>(dst) = H4;
+        *reinterpret_cast<uint4*>(dst + lo_off) = L4;
+      }
+      tc::fence_async_smem();  // operand tiles visible to the tensor core
+    }
     // dh_next = dz @ Wh.T in gate-column order; both sequences share the
     // Wh loads, dz pairs as 16-byte broadcasts
     {
@@ -475,6 +626,76 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
       if (t < Tq[1]) dh_next[1] = acc1;
     }
     __syncthreads();
+    if constexpr (kTc) {
+      if (tid == 0) {
+        // 3xTF32: A_hi B_hi + A_lo B_hi + A_hi B_lo, two K = 8 steps each
+        tc::fence_after();
+        const uint32_t ab = tc::smem_u32(tcbuf + (t & 1) * TC_BUF), bb = ab + 2 * TC_A_BYTES;
+#pragma unroll
+        for (int pr = 0; pr < 3; ++pr) {
+          const uint32_t a0 = ab + (pr == 1 ? TC_A_BYTES : 0), b0 = bb + (pr == 2 ? TC_B_BYTES : 0);
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            mma_tf32(S.tmem, tc::umma_desc(a0 + k * 2 * TC_CS_A, TC_CS_A, 128),
+                     tc::umma_desc(b0 + k * 2 * TC_CS_B, TC_CS_B, 128), (n_issued > 0 || pr > 0 || k > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(&S.bar[t & 1]);
+      }
+      pending |= 1u << (t & 1);
+      ++n_issued;
+    }
+  }
+  if constexpr (kTc) {
+    // this CTA's weight-gradient partial: D (TMEM, fp32) -> dWx, dWh, db;
+    // dw and db_out summed in fp64 over the CTA's sequences in fixed order
+    double* out = a.partial + (int64_t)blockIdx.x * L.n;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // S.xh is no operand source any more (tiles built)
+      S.xh[warp + 8 * q][lane] = dw_acc[q];
+      if (lane == 0) S.xh[warp + 8 * q][40] = g0 + warp + 8 * q < a.B ? fmul((double)Tq[q], d_raw[q]) : 0.0;
+    }
+    // drain the (up to two) outstanding commits
+#pragma unroll
+    for (int bf = 0; bf < 2; ++bf)
+      if ((pending >> bf) & 1u) tc::mbar_wait(&S.bar[bf], (phase >> bf) & 1u);
+    if (n_issued) tc::fence_after();
+    __syncthreads();
+    if (tid < GG) {
+      const int m = tid;  // gate column = TMEM lane (warp w reads lanes 32w..32w+31)
+      if (n_issued) {
+        const uint32_t la = S.tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+        for (int c8 = 0; c8 < 7; ++c8) {  // columns 0..55 (x, h_prev, ones)
+          float v[8];
+          tc::tmem_ld8(la + c8 * 8, v);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int col = c8 * 8 + u;
+            if (col < 16) out[L.oWx + col * GG + m] = (double)v[u];
+            else if (col < 48) out[L.oWh + (col - 16) * GG + m] = (double)v[u];
+            else if (col == 48) out[L.ob + m] = (double)v[u];
+          }
+        }
+      } else {
+        for (int k = 0; k < GK; ++k) out[k * GG + m] = 0.0;
+        out[L.ob + m] = 0.0;
+      }
+    } else if (tid < GG + GH) {
+      const int j = tid - GG;
+      double acc = 0.0;
+      for (int s2 = 0; s2 < GS; ++s2) acc = fadd(acc, S.xh[s2][j]);
+      out[L.ow + j] = acc;
+    } else if (tid == GG + GH) {
+      double acc = 0.0;
+      for (int s2 = 0; s2 < GS; ++s2) acc = fadd(acc, S.xh[s2][40]);
+      out[L.obout] = acc;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem), "r"(TCN) : "memory");
   }
 }
 

@@ -9,6 +9,12 @@ gradient computed on the device (ts_train_grads: cached forward + BPTT +
 weight-gradient reduction, fp64) and the update applied on the device
 (ts_train_apply).  Parameters stay resident between steps.
 
+`mode`: "exact" (default) keeps every gradient in fp64, the reference's
+trajectory; "tc" keeps the fp64 forward/BPTT recurrences and computes the
+weight-gradient contraction on the tensor cores (3xTF32, fused into BPTT,
+ts_train_set_mode(TS_TRAIN_TC)) - gradients within ~1e-5 relative of the
+exact ones (tested), not bit-identical.
+
 Data parallel: pass `dist` (an initialised torch.distributed default group).
 Each rank takes a contiguous shard of every (length-sorted) global
 minibatch, computes its gradient with d_raw divided by the GLOBAL batch size,
@@ -46,6 +52,9 @@ def unflat_into(params, flat: np.ndarray):
     return params
 
 
+TRAIN_MODES = {"exact": 0, "tc": 1}  # TS_TRAIN_EXACT, TS_TRAIN_TC
+
+
 def shard(batch: np.ndarray, rank: int, world: int) -> np.ndarray:
     """Contiguous shard of a global minibatch (sizes differ by at most one)."""
     n = len(batch)
@@ -60,9 +69,10 @@ class DeviceGradients:
     Host form: per-sample normalized matrices (full depth).  Device form
     (`from_device`): shared scheduled rows + prefix depths (bench)."""
 
-    def __init__(self, ctx, X, Tlen, logt, hidden):
+    def __init__(self, ctx, X, Tlen, logt, hidden, mode="exact"):
         self.ctx = ctx
         self.hidden = hidden
+        self.mode = mode
         self.n_params = 16 * 4 * hidden + hidden * 4 * hidden + 4 * hidden + hidden + 1
         if X is None:
             return
@@ -78,14 +88,22 @@ class DeviceGradients:
             ctx.h, _lib._p(rows), rows.shape[0], None, 0, _lib._p(base), _lib._p(zeros),
             _lib._p(T), _lib._p(T.copy()), _lib._p(np.ascontiguousarray(logt, dtype=np.float64)),
             len(T), hidden, 0))
+        self.set_mode(mode)
+
+    def set_mode(self, mode):
+        if mode not in TRAIN_MODES:
+            raise ValueError(f"training mode {mode!r} (expected one of {sorted(TRAIN_MODES)})")
+        self.mode = mode
+        self.ctx.check(self.ctx.lib.ts_train_set_mode(self.ctx.h, TRAIN_MODES[mode]))
 
     @classmethod
     def from_device(cls, ctx, d_rows, n_rows, d_init, n_init, d_row_base, d_init_base, d_T, d_depth,
-                    d_logt, N, hidden):
+                    d_logt, N, hidden, mode="exact"):
         self = cls(ctx, None, None, None, hidden)
         c = ctypes.c_void_p
         ctx.check(ctx.lib.ts_train_load(ctx.h, c(d_rows), n_rows, c(d_init), n_init, c(d_row_base),
                                         c(d_init_base), c(d_T), c(d_depth), c(d_logt), N, hidden, 1))
+        self.set_mode(mode)
         return self
 
     def set_params(self, flat):
@@ -137,7 +155,7 @@ def _eval_split(dev, idxs, Tlen, logt_all, target_scale):
     return mse, r2, float(np.median(rel))
 
 
-def train(params, dataset, cfg, device=None, dist=None, return_trace=False):
+def train(params, dataset, cfg, device=None, dist=None, return_trace=False, mode="exact"):
     """Device-trained copy of `params` and the reference's metrics dict."""
     if len(dataset) < 10:
         raise PipelineError(f"dataset too small ({len(dataset)} < 10 entries)")
@@ -163,7 +181,7 @@ def train(params, dataset, cfg, device=None, dist=None, return_trace=False):
     logt = np.log(targets)
 
     ctx = _lib.context(device)
-    dev = DeviceGradients(ctx, X, Tlen, logt, params.hidden)
+    dev = DeviceGradients(ctx, X, Tlen, logt, params.hidden, mode=mode)
     dev.set_params(flat_params(params))
 
     rank, world, gbuf = 0, 1, None
