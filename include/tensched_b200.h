@@ -184,6 +184,21 @@ int ts_check_action(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int
 int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
               ts_decision* out_decisions, int64_t* visited, double* out_best_v);
 
+/* One layer step for an arbitrary parent state (the children
+ * half of greedy_schedule, search.py:97-110): the parent's n_parent decisions
+ * (schedule order) and n_children (<= 4096) candidate decisions for its next
+ * stage (checked like check_action, schedule_space.py:288-347).  Only the new
+ * row of every child is featurized; bit-identical rows are scored once; the
+ * exact LSTM runs from the shared unscheduled prefix over the T - s timesteps
+ * a child differs in.  out_v (optional, [n_children]): noise-free V of every
+ * child.  out_best (optional): argmin by (V * (1 + U(-eps, eps)), index)
+ * with one splitmix64 draw per child from *rng_state (advanced by
+ * n_children when eps > 0); out_best_v its (noisy) value.  At least one of
+ * out_v / out_best. */
+int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, int64_t n_parent,
+                      const ts_decision* children, int64_t n_children, double epsilon, uint64_t* rng_state,
+                      double* out_v, int64_t* out_best, double* out_best_v);
+
 /* Device-side random partial states (the synthetic sweep generator): state i
  * walks uniformly over candidate_actions with SearchRng(seed0 + i) after
  * drawing its depth d = randrange(T) + 1 (search.py:136-142 variant).

@@ -1286,6 +1286,129 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   return TS_OK;
 }
 
+// One greedy layer for an arbitrary parent: the children's new rows, dedup,
+// the exact LSTM from the shared unscheduled prefix over only the T - s
+// timesteps a child differs in, then V per child and/or the (noisy) argmin.
+int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, int64_t n_parent,
+                      const ts_decision* children, int64_t n_children, double epsilon, uint64_t* rng_state,
+                      double* out_v, int64_t* out_best, double* out_best_v) {
+  if (!ctx || (n_parent > 0 && !parent) || !children || n_parent < 0 || n_children < 1) return TS_ERR_ARG;
+  if (!out_v && !out_best) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (epsilon > 0.0 && !rng_state) return fail(ctx, TS_ERR_ARG, "noisy evaluation needs an rng");
+  if (n_children > 4096) return fail(ctx, TS_ERR_ARG, "more than 4096 children");
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  if (n_parent >= T) return fail(ctx, TS_ERR_ILLEGAL, "state is already complete");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  // host: the parent's nests (legality checked on the way) and the children
+  std::vector<Nest> nests;
+  rc = host_nests(ctx, D, parent, n_parent, nests);
+  if (rc) return rc;
+  const int s = T - 1 - (int)n_parent;
+  const StageDesc& sd = D.st[s];
+  const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
+  const Nest* cn = sd.consumer >= 0 ? &nests[sd.consumer] : nullptr;
+  for (int64_t i = 0; i < n_children; ++i) {
+    const char* why = check_decision(sd, cs, cn, children[i]);
+    if (why) return fail(ctx, TS_ERR_ILLEGAL, why);
+  }
+  const int n = (int)n_children, d = (int)n_parent;
+  // device: state rows = init rows + the parent's featurized rows
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * (T + std::max(d, 1)) * F));
+  double* state_rows = ctx->tmp.as<double>();
+  double* prow = state_rows + (int64_t)T * F;
+  TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * (4096 + T) + sizeof(Nest) + sizeof(int64_t) * 2));
+  ts_decision* hs = ctx->h_stage.as<ts_decision>();
+  memcpy(hs, children, sizeof(ts_decision) * n);
+  if (d) memcpy(hs + 4096, parent, sizeof(ts_decision) * d);
+  Nest* hn = reinterpret_cast<Nest*>(hs + 4096 + T);
+  if (cn) *hn = *cn;
+  int64_t* hoff = reinterpret_cast<int64_t*>(hn + 1);
+  hoff[0] = 0;
+  hoff[1] = d;
+  TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n + T)));
+  TS_CUDA(ctx->rows.reserve(sizeof(double) * F * n));
+  TS_CUDA(ctx->reps.reserve(sizeof(int) * n));
+  TS_CUDA(ctx->raw.reserve(sizeof(double) * 2 * n));
+  TS_CUDA(ctx->out.reserve(sizeof(double) * 2 + sizeof(int64_t) * 2));
+  TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
+  ts_decision* d_children = ctx->records.as<ts_decision>();
+  ts_decision* d_parent = d_children + n;
+  TS_CUDA(cudaMemcpyAsync(d_children, hs, sizeof(ts_decision) * n, cudaMemcpyHostToDevice, ctx->stream));
+  if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, hn, sizeof(Nest), cudaMemcpyHostToDevice, ctx->stream));
+  if (d) {
+    int64_t* d_off = reinterpret_cast<int64_t*>(ctx->out.as<double>() + 2);
+    TS_CUDA(cudaMemcpyAsync(d_parent, hs + 4096, sizeof(ts_decision) * d, cudaMemcpyHostToDevice, ctx->stream));
+    TS_CUDA(cudaMemcpyAsync(d_off, hoff, sizeof(int64_t) * 2, cudaMemcpyHostToDevice, ctx->stream));
+    k_featurize_rows<double><<<1, 128, slot_smem(P, 128), ctx->stream>>>(
+        P->d.as<PipelineDesc>(), d_parent, d_off, 1, P->init_norm.as<double>(), ctx->mean.as<double>(),
+        ctx->stdv.as<double>(), prow, ctx->status.as<int>());
+    TS_LAUNCHED();
+    k_parent_rows<<<(d * F + 127) / 128, 128, 0, ctx->stream>>>(prow, d, T, state_rows);
+    TS_LAUNCHED();
+  }
+  k_children_rows<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+      P->d.as<PipelineDesc>(), s, d_children, n, ctx->nest.as<Nest>(), P->init_raw.as<double>(),
+      ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>());
+  TS_LAUNCHED();
+  k_dedup<<<1, 512, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
+  TS_LAUNCHED();
+  double* raw = ctx->raw.as<double>();
+  if (ctx->hidden == 32) {
+    const size_t xs_bytes = sizeof(double) * F * (T - s);
+    if (xs_bytes > 48 * 1024)
+      TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)xs_bytes));
+    k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
+                                                           ctx->rows.as<double>(), ctx->reps.as<int>(), n,
+                                                           state_rows, raw);
+  } else {
+    k_children_exact<<<(n * 32 + 127) / 128, 128, 0, ctx->stream>>>(
+        lstm_weights(ctx), P->pre_exact.as<double>(), T, s, ctx->rows.as<double>(), ctx->reps.as<int>(), n,
+        state_rows, raw);
+  }
+  TS_LAUNCHED();
+  TS_CUDA(ctx->h_out.reserve(sizeof(double) * (2 + n) + sizeof(int)));
+  double* ho = ctx->h_out.as<double>();
+  if (out_v) {
+    double* dv = raw + n;
+    k_children_v<<<(n + 127) / 128, 128, 0, ctx->stream>>>(raw, ctx->reps.as<int>(), n, ctx->target_scale, dv);
+    TS_LAUNCHED();
+    TS_CUDA(cudaMemcpyAsync(ho + 2, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  const uint64_t rng = rng_state ? *rng_state : 0;
+  if (out_best) {
+    k_argmin<<<1, 1024, 0, ctx->stream>>>(raw, ctx->reps.as<int>(), n, ctx->target_scale, epsilon, rng,
+                                          ctx->out.as<double>());
+    TS_LAUNCHED();
+    TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  int* hst = reinterpret_cast<int*>(ho + 2 + n);
+  TS_CUDA(cudaMemcpyAsync(hst, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (*hst) {
+    const int st = *hst;
+    cudaMemset(ctx->status.p, 0, sizeof(int));
+    return fail(ctx, st, std::string("device: ") + status_name(st));
+  }
+  if (out_v) memcpy(out_v, ho + 2, sizeof(double) * n);
+  if (out_best) {
+    const int best = (int)ho[1];
+    if (best < 0 || best >= n) return fail(ctx, TS_ERR_CUDA, "argmin produced no index");
+    *out_best = best;
+    if (out_best_v) *out_best_v = ho[0];
+    if (rng_state && epsilon > 0.0) *rng_state = rng + (uint64_t)n * 0x9E3779B97F4A7C15ull;
+  }
+  return TS_OK;
+}
+
 int ts_featurize_rows_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_records,
                              const int64_t* d_offsets, int64_t n_states, double* d_rows) {
   if (!ctx || !d_records || !d_offsets || !d_rows || n_states < 0) return TS_ERR_ARG;

@@ -126,7 +126,7 @@ class _PipelineInfo:
         for st in self.stages:
             cons = consumers_of(p, st.name)
             self.sole.append(cons[0] if len(cons) == 1 else None)
-        self.enc_cache = {}   # id(decision) -> (decision, bytes)
+        self.enc_cache = {}   # id(decision) -> (decision, bytes, schedule index)
 
     def loop_table(self, st, split):
         table = {}
@@ -142,7 +142,7 @@ class _PipelineInfo:
 
     def encode(self, idx: int, d) -> bytes:
         hit = self.enc_cache.get(id(d))
-        if hit is not None and hit[0] is d:
+        if hit is not None and hit[0] is d and hit[2] == idx:  # a record is only valid at its stage
             return hit[1]
         st = self.stages[idx]
         if d.stage != st.name:
@@ -194,7 +194,7 @@ class _PipelineInfo:
                 flags |= FLAG_STORE_AT
         rec["flags"] = flags
         b = rec.tobytes()
-        self.enc_cache[id(d)] = (d, b)
+        self.enc_cache[id(d)] = (d, b, idx)
         return b
 
     def decode(self, idx: int, rec) -> LayerSchedule:
@@ -366,7 +366,7 @@ def candidate_actions(s):
     out = []
     for r in buf[: n.value]:
         d = inf.decode(idx, r)
-        inf.enc_cache[id(d)] = (d, r.tobytes())
+        inf.enc_cache[id(d)] = (d, r.tobytes(), idx)
         out.append(d)
     return out
 

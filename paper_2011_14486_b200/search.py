@@ -6,6 +6,11 @@ fused device greedy.
 * `greedy_schedule(p, V, noise, rng)` - the reference loop (search.py:90-112)
   over any V-callable; children are built without re-checking legality
   because they come from candidate_actions.
+* `score_children(params, s, actions)` - V of every child of one parent
+  (ts_score_children): only the new row of each child is featurized and the
+  LSTM runs over only the timesteps the children differ in.  V-callables from
+  `model_value` carry it, and greedy_schedule / beam_search use it for the
+  children of each parent (bit-identical to predict_states on the children).
 * `greedy_schedule_gpu(p, params, noise, rng)` - the fused path: per layer
   the native driver enumerates candidates, the device featurizes only the
   new row of every child, dedups identical rows, runs the exact LSTM from
@@ -67,7 +72,47 @@ class NoiseConfig:
 def model_value(params, jobs: int = 1, mode: int = MODE_EXACT):
     def fn(states):
         return predict_states(params, states, jobs=jobs, mode=mode)
+    if mode == MODE_EXACT:
+        fn.score_children = lambda s, actions: (
+            score_children(params, s, actions) if len(actions) <= 4096
+            else predict_states(params, [child_state(s, a) for a in actions], jobs=jobs, mode=mode))
     return fn
+
+
+def score_children(params, s, actions, noise: NoiseConfig | None = None, rng: SearchRng | None = None,
+                   device=None, best: bool = False):
+    """V (exact, noise-free) of child_state(s, a) for every a in `actions`
+    (legal for s, at most 4096) - or, with best=True, the index and (noisy)
+    value of the argmin by (v * (1 + U(-eps, eps)), index), advancing `rng`
+    by one draw per child like greedy_schedule (search.py:104-110)."""
+    if not actions:
+        raise PipelineError("no children to score")
+    eps = float(noise.epsilon) if noise is not None else 0.0
+    if eps > 0 and rng is None:
+        raise PipelineError("noisy evaluation needs an rng")
+    inf = _info(s.pipeline)
+    ctx = _lib.context(device)
+    ctx.set_params(params)
+    pid = ctx.pipeline_id(inf.desc)
+    parent = np.frombuffer(inf.records_of(s), dtype=_lib.DECISION_DTYPE)
+    pos = len(s.decisions)
+    kids = np.frombuffer(b"".join(inf.encode(pos, a) for a in actions), dtype=_lib.DECISION_DTYPE)
+    st = ctypes.c_uint64(rng.state if rng is not None else 0)
+    if best:
+        bi, bv = ctypes.c_int64(), ctypes.c_double()
+        with ctx.lock:
+            ctx.check(ctx.lib.ts_score_children(ctx.h, pid, _lib._p(parent) if len(parent) else None,
+                                                len(parent), _lib._p(kids), len(kids), eps, ctypes.byref(st),
+                                                None, ctypes.byref(bi), ctypes.byref(bv)))
+        if rng is not None and eps > 0:
+            rng.state = st.value
+        return bi.value, bv.value
+    out = np.empty(len(kids))
+    with ctx.lock:
+        ctx.check(ctx.lib.ts_score_children(ctx.h, pid, _lib._p(parent) if len(parent) else None,
+                                            len(parent), _lib._p(kids), len(kids), 0.0, None,
+                                            _lib._p(out), None, None))
+    return out
 
 
 def table_value(table: dict, default: float = math.inf):
@@ -84,7 +129,8 @@ def greedy_schedule(p, V, noise: NoiseConfig | None = None, rng: SearchRng | Non
         cands = candidate_actions(s)
         visited += len(cands)
         children = [child_state(s, a) for a in cands]
-        vals = [float(v) for v in V(children)]
+        sc = getattr(V, "score_children", None)
+        vals = [float(v) for v in (sc(s, cands) if sc is not None else V(children))]
         if noise is not None and noise.epsilon > 0:
             if rng is None:
                 raise PipelineError("noisy evaluation needs an rng")
@@ -128,9 +174,15 @@ def beam_search(prefix, V, width: int = 8):
     frontier = [prefix]
     while not frontier[0].is_complete:
         children = []
+        sc = getattr(V, "score_children", None)
+        vals = []
         for s in frontier:
-            children.extend(child_state(s, a) for a in candidate_actions(s))
-        vals = V(children)
+            cands = candidate_actions(s)
+            children.extend(child_state(s, a) for a in cands)
+            if sc is not None:
+                vals.extend(sc(s, cands))
+        if sc is None:
+            vals = V(children)
         ranked = sorted(range(len(children)), key=lambda i: (float(vals[i]), i))
         frontier = [children[i] for i in ranked[:width]]
     vals = V(frontier)
