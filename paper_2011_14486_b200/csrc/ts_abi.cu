@@ -794,10 +794,13 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, co
 // ---- packed wire format (8-byte decisions + u8 depths) for host callers
 __constant__ uint8_t c_split_table[16] = {0, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 48, 64, 128, 255};
 
-__global__ void k_depths_to_counts(const uint8_t* __restrict__ depth, int64_t n, int64_t* __restrict__ off) {
+// off[0] = base, off[i + 1] = depth[i] (+ base for i = 0): an inclusive scan
+// of off[1..n] then gives the offsets of a chunk whose records start at base
+__global__ void k_depths_to_counts(const uint8_t* __restrict__ depth, int64_t n, int64_t* __restrict__ off,
+                                   int64_t base = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) off[i + 1] = depth[i];
-  if (i == 0) off[0] = 0;
+  if (i < n) off[i + 1] = depth[i] + (i == 0 ? base : 0);
+  if (i == 0) off[0] = base;
 }
 
 __global__ void k_unpack(const uint64_t* __restrict__ packed, int64_t n, ts_decision* __restrict__ out) {
@@ -934,58 +937,62 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     }
   }
   const int64_t n_chunks = (int64_t)st_at.size() - 1;
-  std::vector<int64_t> rec_at(n_chunks + 1);
-  {
-    int64_t acc = 0;
-    for (int64_t k = 0; k < n_chunks; ++k) {
-      rec_at[k] = acc;
-      acc += (int64_t)sum_bytes(depths + st_at[k], st_at[k + 1] - st_at[k]);
-    }
-    rec_at[n_chunks] = acc;
-  }
-  const int64_t n_rec = rec_at[n_chunks];
-  if (n_rec > 0 && !codes) return TS_ERR_ARG;
+  // Each chunk's record count is summed on the host just before its copies
+  // are queued (the copies of earlier chunks are already in flight), and
+  // its offsets are scanned on the device from its own depths with the
+  // host-known base, so the first chunk starts after its own bytes only.
+  const int T = P->h->n_stages;
+  const int64_t rec_cap = n_states * (int64_t)T;  // depths are <= T (checked by the featurizer)
   TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
   TS_CUDA(ctx->out.reserve(sizeof(double) * n_states));
-  TS_CUDA(ctx->tmp2.reserve(sizeof(uint16_t) * (n_rec > 0 ? n_rec : 1) + n_states + 64));
+  TS_CUDA(ctx->tmp2.reserve(sizeof(uint16_t) * (rec_cap > 0 ? rec_cap : 1) + n_states + 64));
   uint16_t* d_codes = ctx->tmp2.as<uint16_t>();
-  uint8_t* d_depth = reinterpret_cast<uint8_t*>(ctx->tmp2.as<uint8_t>() + ((sizeof(uint16_t) * n_rec + 15) & ~15ull));
+  uint8_t* d_depth = reinterpret_cast<uint8_t*>(ctx->tmp2.as<uint8_t>() + ((sizeof(uint16_t) * rec_cap + 15) & ~15ull));
   int64_t* d_off = ctx->offsets.as<int64_t>();
-  TS_CUDA(cudaMemcpyAsync(d_depth, depths, n_states, cudaMemcpyHostToDevice, ctx->copy_stream));
+  if (!P->code_table.p) {  // every code of every stage, decoded once per pipeline
+    TS_CUDA(P->code_table.reserve(sizeof(ts_decision) * (size_t)T * (TS_CODE_SPACE + 1)));
+    k_code_table<<<(unsigned)((T * (TS_CODE_SPACE + 1) + 255) / 256), 256, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), T, P->code_table.as<ts_decision>());
+    TS_LAUNCHED();
+  }
+  size_t scan_temp = 0;
+  TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_temp, d_off + 1, d_off + 1,
+                                        std::max<int64_t>(first, st_at.size() > 2 ? st_at[2] - st_at[1] : 1),
+                                        ctx->stream));
+  TS_CUDA(ctx->scan_tmp.reserve(scan_temp + 16));
   std::vector<cudaEvent_t> ev;
-  cudaEvent_t dep = take_event(ctx);
-  TS_CUDA(cudaEventRecord(dep, ctx->copy_stream));
-  ev.push_back(dep);
+  int64_t n_rec = 0;
   for (int64_t k = 0; k < n_chunks; ++k) {
-    const int64_t r0 = rec_at[k], r1 = rec_at[k + 1];
+    const int64_t s0 = st_at[k], s1 = st_at[k + 1];
+    const int64_t r0 = n_rec, r1 = r0 + (int64_t)sum_bytes(depths + s0, s1 - s0);
+    if (r1 > rec_cap || (r1 > r0 && !codes)) {
+      cudaStreamSynchronize(ctx->copy_stream);  // no copy may outlive the caller's buffers
+      cudaStreamSynchronize(ctx->stream);
+      return fail(ctx, TS_ERR_ARG, r1 > rec_cap ? "state depth exceeds the pipeline's stage count" : "no codes");
+    }
+    n_rec = r1;
+    TS_CUDA(cudaMemcpyAsync(d_depth + s0, depths + s0, s1 - s0, cudaMemcpyHostToDevice, ctx->copy_stream));
     if (r1 > r0)
       TS_CUDA(cudaMemcpyAsync(d_codes + r0, codes + r0, sizeof(uint16_t) * (r1 - r0), cudaMemcpyHostToDevice,
                               ctx->copy_stream));
     cudaEvent_t in = take_event(ctx);
     ev.push_back(in);
     TS_CUDA(cudaEventRecord(in, ctx->copy_stream));
-  }
-  if (!P->code_table.p) {  // every code of every stage, decoded once per pipeline
-    const int T = P->h->n_stages;
-    TS_CUDA(P->code_table.reserve(sizeof(ts_decision) * (size_t)T * (TS_CODE_SPACE + 1)));
-    k_code_table<<<(unsigned)((T * (TS_CODE_SPACE + 1) + 255) / 256), 256, 0, ctx->stream>>>(
-        P->d.as<PipelineDesc>(), T, P->code_table.as<ts_decision>());
+    TS_CUDA(cudaStreamWaitEvent(ctx->stream, in, 0));
+    // offsets of this chunk: off[s0] = r0 (the previous chunk's scan, or 0)
+    k_depths_to_counts<<<(unsigned)((s1 - s0 + 255) / 256), 256, 0, ctx->stream>>>(d_depth + s0, s1 - s0,
+                                                                                     d_off + s0, r0);
     TS_LAUNCHED();
-  }
-  TS_CUDA(cudaStreamWaitEvent(ctx->stream, dep, 0));
-  k_depths_to_counts<<<(unsigned)((n_states + 255) / 256), 256, 0, ctx->stream>>>(d_depth, n_states, d_off);
-  TS_LAUNCHED();
-  {
-    size_t temp = 0;
-    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + 1, d_off + 1, n_states, ctx->stream));
-    TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
-    TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, d_off + 1, d_off + 1, n_states, ctx->stream));
+    size_t temp = scan_temp;
+    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0, ctx->stream));
+    if (temp > scan_temp) {
+      TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
+      scan_temp = temp;
+    }
+    TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0,
+                                          ctx->stream));
     ++ctx->launches;
-  }
-  for (int64_t k = 0; k < n_chunks; ++k) {
-    const int64_t s0 = st_at[k], s1 = st_at[k + 1];
-    TS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k + 1], 0));
-    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, n_rec, mode,
+    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, r1, mode,
                       ctx->out.as<double>() + s0, d_codes);
     if (rc) return rc;
     cudaEvent_t done = take_event(ctx);
