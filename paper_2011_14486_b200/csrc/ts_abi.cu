@@ -132,7 +132,34 @@ struct ts_ctx {
       tr_pvalid;
   DevBuf tile_ctr;  // k_lstm_tc's dynamic tile counter
   tr::Data tr_data{};
+  // second scoring lane (coded wire path, FAST): alternate chunks run on
+  // their own stream with their own scratch, so one chunk's kernels fill
+  // the SMs the other chunk's kernel tails leave idle
+  cudaStream_t stream2 = nullptr;
+  DevBuf reps2, rows2, tile_ctr2, scan_tmp2;
 };
+
+namespace {
+void swap_buf(DevBuf& a, DevBuf& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.bytes, b.bytes);
+}
+// Swaps the second lane's stream and scratch into the context for a scope.
+struct LaneSwap {
+  ts_ctx* c;
+  bool on;
+  LaneSwap(ts_ctx* ctx, bool alt) : c(ctx), on(alt) { swap_all(); }
+  ~LaneSwap() { swap_all(); }
+  void swap_all() {
+    if (!on) return;
+    std::swap(c->stream, c->stream2);
+    swap_buf(c->reps, c->reps2);
+    swap_buf(c->rows, c->rows2);
+    swap_buf(c->tile_ctr, c->tile_ctr2);
+    swap_buf(c->scan_tmp, c->scan_tmp2);
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -393,9 +420,11 @@ void ts_ctx_destroy(ts_ctx* ctx) {
   if (ctx->d2h_stream) cudaStreamSynchronize(ctx->d2h_stream);
   ctx->pipes.clear();
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
-  cudaStream_t s = ctx->stream, c = ctx->copy_stream, o = ctx->d2h_stream;
+  if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
+  cudaStream_t s = ctx->stream, c = ctx->copy_stream, o = ctx->d2h_stream, s2 = ctx->stream2;
   delete ctx;
   if (s) cudaStreamDestroy(s);
+  if (s2) cudaStreamDestroy(s2);
   if (c) cudaStreamDestroy(c);
   if (o) cudaStreamDestroy(o);
 }
@@ -955,15 +984,21 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
         P->d.as<PipelineDesc>(), T, P->code_table.as<ts_decision>());
     TS_LAUNCHED();
   }
-  size_t scan_temp = 0;
-  TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, scan_temp, d_off + 1, d_off + 1,
-                                        std::max<int64_t>(first, st_at.size() > 2 ? st_at[2] - st_at[1] : 1),
-                                        ctx->stream));
-  TS_CUDA(ctx->scan_tmp.reserve(scan_temp + 16));
   std::vector<cudaEvent_t> ev;
+  // FAST: chunks alternate between two lanes (the exact leg indexes its rows
+  // by global record offsets, so it stays on one lane)
+  const bool two_lanes = mode == TS_MODE_FAST && n_chunks > 1 && !getenv("TS_ONE_LANE");
+  if (two_lanes) {
+    if (!ctx->stream2) TS_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    cudaEvent_t setup = take_event(ctx);  // code table, prefix: issued on lane 0
+    ev.push_back(setup);
+    TS_CUDA(cudaEventRecord(setup, ctx->stream));
+    TS_CUDA(cudaStreamWaitEvent(ctx->stream2, setup, 0));
+  }
   int64_t n_rec = 0;
   for (int64_t k = 0; k < n_chunks; ++k) {
     const int64_t s0 = st_at[k], s1 = st_at[k + 1];
+    LaneSwap lane(ctx, two_lanes && (k & 1));
     const int64_t r0 = n_rec, r1 = r0 + (int64_t)sum_bytes(depths + s0, s1 - s0);
     if (r1 > rec_cap || (r1 > r0 && !codes)) {
       cudaStreamSynchronize(ctx->copy_stream);  // no copy may outlive the caller's buffers
@@ -983,17 +1018,16 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     k_depths_to_counts<<<(unsigned)((s1 - s0 + 255) / 256), 256, 0, ctx->stream>>>(d_depth + s0, s1 - s0,
                                                                                      d_off + s0, r0);
     TS_LAUNCHED();
-    size_t temp = scan_temp;
+    size_t temp = 0;
     TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0, ctx->stream));
-    if (temp > scan_temp) {
-      TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
-      scan_temp = temp;
-    }
+    TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
     TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0,
                                           ctx->stream));
     ++ctx->launches;
-    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0, r1, mode,
-                      ctx->out.as<double>() + s0, d_codes);
+    // FAST rows are chunk-local (decision-major by rowoff); the exact leg's
+    // are indexed by global record offsets
+    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0,
+                      mode == TS_MODE_FAST ? r1 - r0 : r1, mode, ctx->out.as<double>() + s0, d_codes);
     if (rc) return rc;
     cudaEvent_t done = take_event(ctx);
     ev.push_back(done);
