@@ -389,6 +389,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_featurize_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                max_slot_smem);
+
     if (e != cudaSuccess) {
       delete ctx;
       return TS_ERR_CUDA;
@@ -972,7 +973,9 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
   // host-known base, so the first chunk starts after its own bytes only.
   const int T = P->h->n_stages;
   const int64_t rec_cap = n_states * (int64_t)T;  // depths are <= T (checked by the featurizer)
-  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
+  // chunk k owns offsets d_off[s0 + k .. s1 + k] (its own first entry, so no
+  // two chunks - possibly on different lanes - ever touch the same word)
+  TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + n_chunks + 1)));
   TS_CUDA(ctx->out.reserve(sizeof(double) * n_states));
   TS_CUDA(ctx->tmp2.reserve(sizeof(uint16_t) * (rec_cap > 0 ? rec_cap : 1) + n_states + 64));
   uint16_t* d_codes = ctx->tmp2.as<uint16_t>();
@@ -1014,19 +1017,19 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     ev.push_back(in);
     TS_CUDA(cudaEventRecord(in, ctx->copy_stream));
     TS_CUDA(cudaStreamWaitEvent(ctx->stream, in, 0));
-    // offsets of this chunk: off[s0] = r0 (the previous chunk's scan, or 0)
+    // offsets of this chunk: off_k[0] = r0, then the scan of its depths
+    int64_t* off_k = d_off + s0 + k;
     k_depths_to_counts<<<(unsigned)((s1 - s0 + 255) / 256), 256, 0, ctx->stream>>>(d_depth + s0, s1 - s0,
-                                                                                     d_off + s0, r0);
+                                                                                     off_k, r0);
     TS_LAUNCHED();
     size_t temp = 0;
-    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0, ctx->stream));
+    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
     TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
-    TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, d_off + s0 + 1, d_off + s0 + 1, s1 - s0,
-                                          ctx->stream));
+    TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
     ++ctx->launches;
     // FAST rows are chunk-local (decision-major by rowoff); the exact leg's
     // are indexed by global record offsets
-    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_off + s0, s1 - s0,
+    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), off_k, s1 - s0,
                       mode == TS_MODE_FAST ? r1 - r0 : r1, mode, ctx->out.as<double>() + s0, d_codes);
     if (rc) return rc;
     cudaEvent_t done = take_event(ctx);

@@ -245,7 +245,9 @@ def test_coded_wire_format_matches(gpu_ctx, v0):
         a = np.empty(n)
         gpu_ctx.check(gpu_ctx.lib.ts_score_states(gpu_ctx.h, pid, _lib._p(h_recs), _lib._p(h_offs), n, mode,
                                                   _lib._p(a)))
-        for chunk, step in ((None, None), ("50000", None), ("20000", "45000")):
+        # many small chunks alternate between the two scoring lanes (FAST):
+        # every chunk must own its offsets and scratch
+        for chunk, step in ((None, None), ("50000", None), ("20000", "45000"), ("4096", "6000")):
             if chunk:
                 os.environ["TS_CODED_CHUNK"] = chunk
             if step:
