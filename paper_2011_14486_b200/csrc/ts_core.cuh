@@ -284,7 +284,8 @@ TS_HD double make_double(uint64_t mant, int e2) {
 
 // Round q + f (0 <= f < 1, f > 0 iff sticky) to 53 bits half-even, times
 // 2^e2.  Callers guarantee q has >= 55 bits whenever sticky is set.
-TS_HD_NOINLINE double round_u256(const u256& q, bool sticky, int e2) {
+// (by value: a reference would force the caller's u256 into local memory)
+TS_HD_NOINLINE double round_u256(const u256 q, bool sticky, int e2) {
   const int bl = u256_bitlen(q);
   if (bl == 0) return 0.0;
   if (bl <= 53) {
@@ -358,7 +359,7 @@ TS_HD u256 u256_div(const u256& a, const Divisor& D, bool& inexact) {
 }
 
 // CPython int/int true division (long_true_divide): correctly rounded n/d.
-TS_HD_NOINLINE double u256_div_to_double_slow(const u256& n, const Divisor& D) {
+TS_HD_NOINLINE double u256_div_to_double_slow(const u256 n, const Divisor D) {
   const int a = u256_bitlen(n);
   if (a == 0) return 0.0;
   const int b = 64 - clz64(D.d);
@@ -568,9 +569,12 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn
 
 // _nest_entry/_build_loops (schedule_space.py:228-274).  `cn` may be null
 // for Root decisions; pe receives the per-invocation pure extents.
+// inner_out (optional): the innermost loop's extent, taken from the value
+// being stored (a later lookup ext[n_loops - 1] is a dynamic index, which
+// would pin the Nest in local memory on the device).
 template <class CN = Nest>
 TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, const ts_decision& d,
-                     Nest& out, int64_t* pe) {
+                     Nest& out, int64_t* pe, uint32_t* inner_out = nullptr) {
   if (d.anchor >= 0) {
     if (!cn || !cs || d.anchor >= cn->loops()) return TS_ERR_ILLEGAL;
     const int rc = anchored_extents(s, *cs, *cn, d.anchor, pe, out.inv, out.depth);
@@ -584,6 +588,7 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, cons
   if (d.n_loops == 0 || d.n_loops > TS_MAX_LOOPS) return TS_ERR_ILLEGAL;
   out.n_loops = d.n_loops;
   bool bad = false;
+  uint32_t inner = 0;
   uint32_t split4;  // split factors, a byte per pure dim
   memcpy(&split4, d.split, 4);
 #pragma unroll
@@ -609,7 +614,9 @@ TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, cons
                                                                             : s.ext[s.n_pure + 3];
     }
     out.ext[j] = (uint32_t)e;
+    if (j == d.n_loops - 1) inner = (uint32_t)e;
   }
+  if (inner_out) *inner_out = inner;
   return bad ? TS_ERR_ILLEGAL : TS_OK;
 }
 
@@ -765,11 +772,7 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
 // Acquired features f8..f15 of a scheduled stage (featurizer.py:86-103),
 // raw (not normalized).
 TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe, const ts_decision& d,
-                            double* f) {
-  uint32_t inner = 0;
-#pragma unroll
-  for (int j = 0; j < TS_MAX_LOOPS; ++j)
-    if (j == n.n_loops - 1) inner = n.ext[j];
+                            double* f, uint32_t inner) {
   f[0] = 1.0;
   f[1] = log2_int(d.vec);
   f[2] = (d.flags & TS_FLAG_PARALLEL) ? log2_int(n.ext[0]) : 0.0;
@@ -813,6 +816,15 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
     f[7] = glibc_log2(u256_to_double(inv1));
   }
   return TS_OK;
+}
+
+TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe, const ts_decision& d,
+                            double* f) {
+  uint32_t inner = 0;
+#pragma unroll
+  for (int j = 0; j < TS_MAX_LOOPS; ++j)
+    if (j == n.n_loops - 1) inner = n.ext[j];
+  return acquired_features(s, n, pe, d, f, inner);
 }
 
 // Intrinsic features f0..f7 (featurizer.py:44-65).
