@@ -467,10 +467,10 @@ def main():
     avg = {names[k]: times[k] / counts[k] for k in range(4) if counts[k]}
     dom = max(avg, key=lambda k: times[names.index(k)])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    # ncu --set full capture (profiles/r01_ncu.md): DRAM bytes per state of each
-    # kernel at 2^20 states, scaled to this launch
-    traffic_per_state = {"featurize": (449.214208e6 + 572.307200e6) / 1048576,
-                         "lstm_fast": (633.981696e6 + 17.002240e6) / 1048576}
+    # ncu --set full captures (profiles/r01_ncu.md): DRAM bytes per state of each
+    # kernel at 12.5M states (this bench's default launch), scaled to this launch
+    traffic_per_state = {"featurize": (6.281158e9 + 6.988932e9) / 12.5e6,
+                         "lstm_fast": (8.768533e9 + 0.394084e9) / 12.5e6}
     row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
         bytes_per_launch = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
@@ -492,9 +492,19 @@ def main():
                 "traffic": tr * M if tr else None, "flops_per_launch": flops_per_launch,
                 "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
     roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
-    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 76%, "
-                    "issue 64% in ncu), k_featurize_rows is ALU/issue-bound integer work (ALU 50%, issue 61%); "
-                    "profiles/r01_ncu.md")
+    if "lstm_fast" in avg:
+        # the LSTM's binding unit: 5 ex2 + 1 rcp per hidden unit and
+        # timestep (pairs of units share a reciprocal) = 192 MUFU ops per
+        # state-timestep against 16 MUFU ops/clk/SM
+        mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965
+        mufu_peak = 16 * (torch.cuda.get_device_properties(dev).multi_processor_count) * mhz * 1e6
+        mufu = 192.0 * timesteps / (avg["lstm_fast"] / 1e3)
+        roof["k_lstm_tc_mufu"] = {"bound": "xu (MUFU)", "achieved": mufu / 1e12, "peak": mufu_peak / 1e12,
+                                  "unit": "Tops/s", "frac": mufu / mufu_peak,
+                                  "algorithmic": "192 MUFU ops per state-timestep (5 ex2 + 1 rcp per unit)"}
+    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 79%, "
+                    "issue 59% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work "
+                    "(ALU 54%, issue 63%); profiles/r01_ncu.md")
 
     train_line = None
     if not args.no_train:
