@@ -7,7 +7,9 @@
 // M=128 rows of one UMMA: D[128 x 128] (fp32, TMEM) = A[128 x K] . B[128 x K]^T
 // with fp16 operands split hi/lo and concatenated along K,
 //     A' = [a_hi | a_lo | a_hi | 1 1 0..0],  B' = [W_hi ; W_hi ; W_lo ; b_hi b_lo 0..0]
-// (K = 3*48 + 16 = 160, ten K=16 UMMAs) so z ~= a_hi W_hi + a_lo W_hi + a_hi W_lo + b
+// (K = 3*48 + 16 = 160, ten K=16 UMMAs; the second a_hi is the first one
+// re-read through the UMMA descriptor, not a copy) so
+// z ~= a_hi W_hi + a_lo W_hi + a_hi W_lo + b
 // with 22-bit operands and fp32 accumulation (|dV|/V <= 1e-4, the north-star
 // fp32 tolerance).  The gate columns of B' are pre-scaled by -log2(e)
 // (i, f, o) and -2 log2(e) (g) so every gate costs one ex2.approx and one
@@ -45,10 +47,18 @@ constexpr int KP = 3 * KA + 16;           // split-concatenated K + bias block =
 constexpr int KCH = KP / 8;               // 16-byte K chunks = 20
 constexpr int KSTEPS = KP / 16;           // UMMAs per timestep = 10
 constexpr int CHUNK_STRIDE = TM * 16;     // bytes between K chunks (LBO) = 2048
-constexpr int TILE_BYTES = KCH * CHUNK_STRIDE;  // 40960 per operand
+constexpr int TILE_BYTES = KCH * CHUNK_STRIDE;  // 40960: the B' weight image
+// A holds a_hi and a_lo once (the third product a_hi.W_lo re-reads a_hi's
+// chunks through its descriptor) plus the bias block: 14 chunks, so every
+// row costs two 16-byte stores per K chunk instead of three
+constexpr int A_KCH = 2 * (KA / 8) + 2;  // 14
+constexpr int A_BYTES = A_KCH * CHUNK_STRIDE;  // 28672
 constexpr int NWG = 4;                    // warpgroups (tiles in flight) per CTA
 constexpr int THREADS = NWG * TM;
-constexpr int SMEM_BYTES = (1 + NWG) * TILE_BYTES + 1024;  // B, NWG x A, readout + barriers
+constexpr int SMEM_BYTES = TILE_BYTES + NWG * A_BYTES + 1024;  // B, NWG x A, readout + barriers
+// A chunk read by UMMA step s (K = 16 = two chunks): a_hi . W_hi (s 0-2),
+// a_lo . W_hi (3-5), a_hi . W_lo (6-8, a_hi again), bias (9)
+__device__ __forceinline__ int a_chunk(int s) { return s < 6 ? 2 * s : s < 9 ? 2 * (s - 6) : 12; }
 constexpr int PRE_STRIDE = 72;            // floats per prefix position: h[32], c[32], raw (f64)
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -156,30 +166,29 @@ __device__ __forceinline__ void st_chunk(uint8_t* A, int kc, int r, const uint4&
 }
 
 // x part, pre-split (x4 = intrinsic hi, lo, acquired hi, lo): chunks q = 0
-// (intrinsic), 1 (acquired) of every segment
+// (intrinsic), 1 (acquired) of the hi and lo segments
 __device__ __forceinline__ void put_x(uint8_t* A, int r, const uint4* x4) {
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     st_chunk(A, 0 * 6 + q, r, x4[2 * q]);
     st_chunk(A, 1 * 6 + q, r, x4[2 * q + 1]);
-    st_chunk(A, 2 * 6 + q, r, x4[2 * q]);
   }
 }
 
-// h part: 8 units of group g8 -> chunk q = 2 + g8 of every segment
+// h part: 8 units of group g8 -> chunk q = 2 + g8 of the hi and lo segments
 __device__ __forceinline__ void put_h8(uint8_t* A, int r, int g8, const float* h8) {
   uint4 hi, lo;
   split8(h8, hi, lo);
   st_chunk(A, 0 * 6 + 2 + g8, r, hi);
   st_chunk(A, 1 * 6 + 2 + g8, r, lo);
-  st_chunk(A, 2 * 6 + 2 + g8, r, hi);
 }
 
-// bias block: K entries 144, 145 = 1.0 (multiplying b_hi, b_lo), rest 0
+// bias block (A chunks 12, 13 against B' K entries 144..159): 1.0, 1.0
+// multiplying b_hi, b_lo, rest 0
 __device__ __forceinline__ void put_bias_ones(uint8_t* A, int r) {
   const uint32_t one_one = 0x3C003C00u;  // two fp16 1.0
-  st_chunk(A, 18, r, make_uint4(one_one, 0u, 0u, 0u));
-  st_chunk(A, 19, r, make_uint4(0u, 0u, 0u, 0u));
+  st_chunk(A, 12, r, make_uint4(one_one, 0u, 0u, 0u));
+  st_chunk(A, 13, r, make_uint4(0u, 0u, 0u, 0u));
 }
 
 // ---------------------------------------------------------------- kernel
@@ -280,8 +289,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   const int wg = tid / TM;            // warpgroup
   const int r = tid % TM;             // row within the tile = TMEM lane
   const int warp = tid >> 5;
-  uint8_t* A = smem + (1 + wg) * TILE_BYTES;
-  float* wout = reinterpret_cast<float*>(smem + (1 + NWG) * TILE_BYTES);  // [32]
+  uint8_t* A = smem + TILE_BYTES + wg * A_BYTES;
+  float* wout = reinterpret_cast<float*>(smem + TILE_BYTES + NWG * A_BYTES);  // [32]
   uint64_t* bars = reinterpret_cast<uint64_t*>(wout + 64);               // [NWG]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
   volatile int* tile_slot = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [NWG]
@@ -365,7 +374,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
         fence_after();
 #pragma unroll
         for (int s = 0; s < KSTEPS; ++s)
-          mma_f16(tmem, umma_desc(a_base + s * 2 * CHUNK_STRIDE, CHUNK_STRIDE, 128),
+          mma_f16(tmem, umma_desc(a_base + a_chunk(s) * CHUNK_STRIDE, CHUNK_STRIDE, 128),
                   umma_desc(b_base + s * 2 * CHUNK_STRIDE, CHUNK_STRIDE, 128), s > 0);
         mma_commit(bar);
       }
