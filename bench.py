@@ -506,6 +506,29 @@ def main():
                     "issue 59% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work "
                     "(ALU 54%, issue 63%); profiles/r01_ncu.md")
 
+    # ---- batch-size sweep (1e4..1e7 states per GPU), device-resident,
+    # on prefixes of this rank's states: where launch latency stops mattering
+    sweep = {}
+    for n_sw in (10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7):
+        if n_sw > M:
+            break
+        nr_sw = int(offs[n_sw].item())
+        out_sw = out[:n_sw]
+
+        def sw_step():
+            ctx.check(ctx.lib.ts_score_states_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), n_sw,
+                                                     nr_sw, mode, out_sw.data_ptr()))
+        sw_step()
+        reps = max(3, min(50, int(2e7 // n_sw)))
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            sw_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        sweep[f"{n_sw:.0e}"] = round(n_sw * reps / (e0.elapsed_time(e1) / 1e3), 1)
+
     train_line = None
     if not args.no_train:
         train_line = train_throughput(ctx, pid, inf, params, rank, world, dev, args)
@@ -513,7 +536,7 @@ def main():
     greedy = {}
     if rank == 0 and not args.no_greedy:
         from paper_2011_14486_b200.search import greedy_schedule_gpu
-        for net in ("resnet18", "resnet50", "mobilenet_v2"):
+        for net in ("crp2d", "resnet18", "resnet50", "mobilenet_v2"):
             pn = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
             greedy_schedule_gpu(pn, params)  # warm (descriptor upload, prefix)
             t0 = time.perf_counter()
@@ -554,6 +577,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "greedy_wall_s": greedy,
+            "sweep_states_per_s": sweep,
             "v_training": train_line,
             "clocks": clk,
         }

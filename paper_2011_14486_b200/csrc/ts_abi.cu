@@ -608,7 +608,12 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   tc::k_init_split<<<(unsigned)((T + 63) / 64), 64, 0, ctx->stream>>>(P->init_norm.as<double>(), T, initx);
   TS_LAUNCHED();
   if (!ctx->tc_attr_set) {
-    TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+    TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem_bytes(4)));
+    TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem_bytes(2)));
+    TS_CUDA(cudaFuncSetAttribute(tc::k_lstm_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem_bytes(1)));
     ctx->tc_attr_set = true;
   }
   tc::TcArgs ta;
@@ -622,7 +627,7 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   ta.b_out = ctx->b_out;
   tc::k_prefix0<<<1, 64, 0, ctx->stream>>>(ta.pre, T, ctx->b_out);
   TS_LAUNCHED();
-  tc::k_lstm_tc<<<1, tc::THREADS, tc::SMEM_BYTES, ctx->stream>>>(ta);
+  tc::k_lstm_tc<4><<<1, 4 * tc::TM, tc::smem_bytes(4), ctx->stream>>>(ta);
   TS_LAUNCHED();
   P->fast_version = ctx->params_version;
   return TS_OK;
@@ -722,8 +727,16 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     ta.tile_counter = ctx->tile_ctr.as<int>();
     {
       KTimer kt(ctx, TS_K_LSTM_FAST);
-      const int grid = std::min((ta.n_tiles + tc::NWG - 1) / tc::NWG, ctx->sm_count);
-      tc::k_lstm_tc<<<grid, tc::THREADS, tc::SMEM_BYTES, ctx->stream>>>(ta);
+      // four tiles per SM when there are enough; fewer per CTA (more SMs)
+      // for small batches
+      const int nwg = ta.n_tiles <= ctx->sm_count ? 1 : ta.n_tiles <= 2 * ctx->sm_count ? 2 : 4;
+      const int grid = std::min((ta.n_tiles + nwg - 1) / nwg, ctx->sm_count);
+      if (nwg == 4)
+        tc::k_lstm_tc<4><<<grid, 4 * tc::TM, tc::smem_bytes(4), ctx->stream>>>(ta);
+      else if (nwg == 2)
+        tc::k_lstm_tc<2><<<grid, 2 * tc::TM, tc::smem_bytes(2), ctx->stream>>>(ta);
+      else
+        tc::k_lstm_tc<1><<<grid, tc::TM, tc::smem_bytes(1), ctx->stream>>>(ta);
       TS_LAUNCHED();
     }
     return TS_OK;

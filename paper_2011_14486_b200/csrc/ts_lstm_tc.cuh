@@ -56,6 +56,7 @@ constexpr int A_BYTES = A_KCH * CHUNK_STRIDE;  // 28672
 constexpr int NWG = 4;                    // warpgroups (tiles in flight) per CTA
 constexpr int THREADS = NWG * TM;
 constexpr int SMEM_BYTES = TILE_BYTES + NWG * A_BYTES + 1024;  // B, NWG x A, readout + barriers
+constexpr int smem_bytes(int nwg) { return TILE_BYTES + nwg * A_BYTES + 1024; }
 // A chunk read by UMMA step s (K = 16 = two chunks): a_hi . W_hi (s 0-2),
 // a_lo . W_hi (3-5), a_hi . W_lo (6-8, a_hi again), bias (9)
 __device__ __forceinline__ int a_chunk(int s) { return s < 6 ? 2 * s : s < 9 ? 2 * (s - 6) : 12; }
@@ -282,7 +283,13 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
+// kNWG warpgroups (tiles in flight) per CTA: 4 for large batches; 1 or 2
+// when there are too few tiles to give every SM four, so small batches use
+// more SMs.  The per-row arithmetic is the same code in every variant (and
+// capped at the same 128 registers), so a state's V does not depend on the
+// batch it is scored in.
+template <int kNWG = NWG>
+__global__ void __launch_bounds__(kNWG * TM, 4 / kNWG) k_lstm_tc(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* B = smem;
   const int tid = threadIdx.x;
@@ -290,26 +297,26 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   const int r = tid % TM;             // row within the tile = TMEM lane
   const int warp = tid >> 5;
   uint8_t* A = smem + TILE_BYTES + wg * A_BYTES;
-  float* wout = reinterpret_cast<float*>(smem + TILE_BYTES + NWG * A_BYTES);  // [32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wout + 64);               // [NWG]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NWG);
-  volatile int* tile_slot = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [NWG]
+  float* wout = reinterpret_cast<float*>(smem + TILE_BYTES + kNWG * A_BYTES);  // [32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wout + 64);               // [kNWG]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNWG);
+  volatile int* tile_slot = reinterpret_cast<volatile int*>(tmem_slot + 1);  // [kNWG]
 
   // weights -> shared (B' image is already in the canonical layout)
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.wpack);
     uint4* dst = reinterpret_cast<uint4*>(B);
-    for (int i = tid; i < TILE_BYTES / 16; i += THREADS) dst[i] = __ldg(src + i);
+    for (int i = tid; i < TILE_BYTES / 16; i += kNWG * TM) dst[i] = __ldg(src + i);
     if (tid < 32) wout[tid] = __ldg(reinterpret_cast<const float*>(a.wpack + TILE_BYTES) + tid);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(NWG * 128)
+                 "r"(kNWG * 128)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int g = 0; g < NWG; ++g) mbar_init(bars + g, 1);
+    for (int g = 0; g < kNWG; ++g) mbar_init(bars + g, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_async_smem();
@@ -325,9 +332,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
   put_bias_ones(A, r);
 
   // Tiles are in descending depth order; each warpgroup starts with one of
-  // the first gridDim*NWG and then takes the next unclaimed tile (longest
+  // the first gridDim*kNWG and then takes the next unclaimed tile (longest
   // first, so the short tail tiles fill the gaps)
-  for (int tile = blockIdx.x * NWG + wg; tile < a.n_tiles;) {
+  for (int tile = blockIdx.x * kNWG + wg; tile < a.n_tiles;) {
     const int64_t sp = (int64_t)tile * TM + r;
     const bool valid = a.record_prefix ? (r == 0) : (sp < a.n);
     int64_t st = 0, off = 0;
@@ -407,19 +414,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_lstm_tc(TcArgs a) {
     }
     if (!a.record_prefix && valid) a.out[st] = exp(fadd(raw, a.target_scale));
     if (a.tile_counter) {
-      if (r == 0) tile_slot[wg] = gridDim.x * NWG + atomicAdd(a.tile_counter, 1);
+      if (r == 0) tile_slot[wg] = gridDim.x * kNWG + atomicAdd(a.tile_counter, 1);
       wg_sync(wg);
       tile = tile_slot[wg];
     } else {
       wg_sync(wg);
-      tile += gridDim.x * NWG;
+      tile += gridDim.x * kNWG;
     }
   }
   fence_before();
   __syncthreads();
   fence_after();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(NWG * 128)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "r"(kNWG * 128)
                  : "memory");
 }
 

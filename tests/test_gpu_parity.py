@@ -168,6 +168,14 @@ def test_fast_mode_large_batch_matches_exact(gpu_ctx, v0):
         out[mode] = o.cpu().numpy()
     assert np.all(out[MODE_EXACT] > 0)
     np.testing.assert_allclose(out[MODE_FAST], out[MODE_EXACT], rtol=FAST_RTOL, atol=0)
+    # batch-size independence across the LSTM kernel's variants (1, 2 or 4
+    # tiles per CTA, chosen by the batch's tile count): prefixes of the batch
+    # give bit-identical FAST values
+    for m in (3_000, 30_000, 100_000):
+        o = torch.empty(m, dtype=torch.float64, device="cuda")
+        gpu_ctx.check(gpu_ctx.lib.ts_score_states_device(gpu_ctx.h, pid, recs.data_ptr(), offs.data_ptr(), m,
+                                                         int(offs[m].item()), MODE_FAST, o.data_ptr()))
+        assert np.array_equal(bits(o.cpu().numpy()), bits(out[MODE_FAST][:m])), m
 
 
 def test_reference_greedy_with_gpu_v_callable(greedy_golden, v0_path):
