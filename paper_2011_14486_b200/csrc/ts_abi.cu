@@ -701,7 +701,8 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     TS_CUDA(ctx->rows.reserve(sizeof(float) * 8 * (n_records > 0 ? n_records : 1)));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
-      k_featurize_rows<float><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
+      k_featurize_rows<float><<<(unsigned)((n_states + TS_FEAT_BLOCK - 1) / TS_FEAT_BLOCK), TS_FEAT_BLOCK,
+                                slot_smem(P, TS_FEAT_BLOCK), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>(),
           perm, rowoff, d_codes);
