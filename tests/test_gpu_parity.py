@@ -66,6 +66,8 @@ def test_greedy_fused_matches_reference(greedy_golden, v0):
         p = pipeline_from(g)
         s, visited, v = greedy_schedule_gpu(p, v0, return_value=True)
         assert [d.render() for d in s.decisions] == g["schedule"], key
+        # the schedule file `cmd_schedule` writes (schedule_space.py:479-481), byte for byte
+        assert ss.write_schedule(s) == "\n".join(g["schedule"]) + "\n", key
         assert visited == g["visited"], key
         assert abs(v / float.fromhex(g["predicted"]) - 1) < EXACT_RTOL, key
 
