@@ -9,8 +9,9 @@ fused device greedy.
 * `score_children(params, s, actions)` - V of every child of one parent
   (ts_score_children): only the new row of each child is featurized and the
   LSTM runs over only the timesteps the children differ in.  V-callables from
-  `model_value` carry it, and greedy_schedule / beam_search use it for the
-  children of each parent (bit-identical to predict_states on the children).
+  `model_value` carry it and greedy_schedule uses it for each layer's
+  children (bit-identical to predict_states on the children); beam_search
+  keeps one predict_states batch per layer for all parents' children.
 * `greedy_schedule_gpu(p, params, noise, rng)` - the fused path: per layer
   the native driver enumerates candidates, the device featurizes only the
   new row of every child, dedups identical rows, runs the exact LSTM from
@@ -173,16 +174,12 @@ def beam_search(prefix, V, width: int = 8):
         raise PipelineError("beam width must be >= 1")
     frontier = [prefix]
     while not frontier[0].is_complete:
+        # one device batch per layer for all parents' children (per-parent
+        # score_children calls would cost one round trip per beam entry)
         children = []
-        sc = getattr(V, "score_children", None)
-        vals = []
         for s in frontier:
-            cands = candidate_actions(s)
-            children.extend(child_state(s, a) for a in cands)
-            if sc is not None:
-                vals.extend(sc(s, cands))
-        if sc is None:
-            vals = V(children)
+            children.extend(child_state(s, a) for a in candidate_actions(s))
+        vals = V(children)
         ranked = sorted(range(len(children)), key=lambda i: (float(vals[i]), i))
         frontier = [children[i] for i in ranked[:width]]
     vals = V(frontier)

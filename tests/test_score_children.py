@@ -66,15 +66,20 @@ def test_children_argmin_with_noise(greedy_golden, v0):
             assert dev_rng.state == (host_rng.state if eps else 77 + i)
 
 
-def test_beam_search_uses_children_path(greedy_golden, v0):
-    """beam_search over model_value (children scored per parent on the
-    device) equals beam_search over a plain predict_states callable."""
+def test_generic_greedy_and_beam_agree_with_plain_callable(greedy_golden, v0):
+    """greedy_schedule over model_value (children through score_children)
+    and beam_search over it equal the same searches over a plain
+    predict_states callable."""
     p = pipeline_from(greedy_golden["ref:pipelines/deep/p12_deep.pl"])
     plain = lambda states: predict_states(v0, states)  # noqa: E731
     for width in (1, 3):
         a = beam_search(ss.initial_state(p), model_value(v0), width)
         b = beam_search(ss.initial_state(p), plain, width)
         assert a.decisions == b.decisions
+    from paper_2011_14486_b200.search import greedy_schedule
+    a, va = greedy_schedule(p, model_value(v0))
+    b, vb = greedy_schedule(p, plain)
+    assert a.decisions == b.decisions and va == vb
 
 
 def test_illegal_child_rejected(greedy_golden, v0):
