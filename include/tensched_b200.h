@@ -163,6 +163,13 @@ int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_re
                            const int64_t* d_offsets, int64_t n_states, int64_t n_records,
                            int mode, double* d_out_v);
 
+/* ts_score_states_coded with device-resident inputs: d_codes (16-bit
+ * action codes, 2 B per decision) and d_offsets (n_states + 1), stream-
+ * ordered on the context stream. */
+int ts_score_states_coded_device(ts_ctx* ctx, int pipeline_id, const uint16_t* d_codes,
+                                 const int64_t* d_offsets, int64_t n_states, int64_t n_records,
+                                 int mode, double* d_out_v);
+
 /* backend.lstm_forward(X, Wx, Wh, b, w, b_out) -> raw (backend.py:26). */
 int ts_lstm_forward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t F,
                     const double* Wx, const double* Wh, const double* b, const double* w,

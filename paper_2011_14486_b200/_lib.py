@@ -123,6 +123,7 @@ def load_library():
             "ts_train_forward": ([vp, vp, i64, vp], i32),
             "ts_train_set_mode": ([vp, i32], i32),
             "ts_score_children": ([vp, i32, vp, i64, vp, i64, f64, vp, vp, vp, vp], i32),
+            "ts_score_states_coded_device": ([vp, i32, vp, vp, i64, i64, i32, vp], i32),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(lib, name)

@@ -1121,6 +1121,29 @@ int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_re
   return check_device_status(ctx);
 }
 
+int ts_score_states_coded_device(ts_ctx* ctx, int pipeline_id, const uint16_t* d_codes, const int64_t* d_offsets,
+                                 int64_t n_states, int64_t n_records, int mode, double* d_out_v) {
+  if (!ctx || !d_offsets || !d_out_v || n_states < 0 || (n_records > 0 && !d_codes)) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (n_states == 0) return TS_OK;
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  if (!P->code_table.p) {  // every code of every stage, decoded once per pipeline
+    const int T = P->h->n_stages;
+    TS_CUDA(P->code_table.reserve(sizeof(ts_decision) * (size_t)T * (TS_CODE_SPACE + 1)));
+    k_code_table<<<(unsigned)((T * (TS_CODE_SPACE + 1) + 255) / 256), 256, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), T, P->code_table.as<ts_decision>());
+    TS_LAUNCHED();
+  }
+  rc = score_device(ctx, P, P->code_table.as<ts_decision>(), d_offsets, n_states, n_records, mode, d_out_v,
+                    d_codes);
+  if (rc) return rc;
+  return check_device_status(ctx);
+}
+
 int ts_lstm_forward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t Fdim, const double* Wx,
                     const double* Wh, const double* b, const double* w, int64_t H, double b_out, int mode,
                     double* raw_out) {

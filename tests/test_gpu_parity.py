@@ -255,6 +255,11 @@ def test_coded_wire_format_matches(gpu_ctx, v0):
         a = np.empty(n)
         gpu_ctx.check(gpu_ctx.lib.ts_score_states(gpu_ctx.h, pid, _lib._p(h_recs), _lib._p(h_offs), n, mode,
                                                   _lib._p(a)))
+        # device-resident codes (ts_score_states_coded_device)
+        d_out = torch.empty(n, dtype=torch.float64, device="cuda")
+        gpu_ctx.check(gpu_ctx.lib.ts_score_states_coded_device(gpu_ctx.h, pid, d_codes.data_ptr(), offs.data_ptr(),
+                                                               n, len(h_recs), mode, d_out.data_ptr()))
+        assert np.array_equal(bits(a), bits(d_out.cpu().numpy())), mode
         # many small chunks alternate between the two scoring lanes (FAST):
         # every chunk must own its offsets and scratch
         for chunk, step in ((None, None), ("50000", None), ("20000", "45000"), ("4096", "6000")):
