@@ -127,6 +127,10 @@ class _PipelineInfo:
             cons = consumers_of(p, st.name)
             self.sole.append(cons[0] if len(cons) == 1 else None)
         self.enc_cache = {}   # id(decision) -> (decision, bytes, schedule index)
+        # (schedule index, decision) -> bytes: decisions are frozen dataclasses,
+        # so equal decisions built by any caller (a foreign search's own
+        # objects) encode once; bounded by the distinct actions per stage
+        self.val_cache = {}
 
     def loop_table(self, st, split):
         table = {}
@@ -144,6 +148,12 @@ class _PipelineInfo:
         hit = self.enc_cache.get(id(d))
         if hit is not None and hit[0] is d and hit[2] == idx:  # a record is only valid at its stage
             return hit[1]
+        try:
+            b = self.val_cache.get((idx, d))
+        except TypeError:  # an unhashable decision-like object
+            b = None
+        if b is not None:
+            return b
         st = self.stages[idx]
         if d.stage != st.name:
             raise IllegalActionError(
@@ -194,7 +204,14 @@ class _PipelineInfo:
                 flags |= FLAG_STORE_AT
         rec["flags"] = flags
         b = rec.tobytes()
+        if len(self.enc_cache) >= (1 << 20):  # bounded: foreign callers bring new objects
+            self.enc_cache.clear()
         self.enc_cache[id(d)] = (d, b, idx)
+        try:
+            if len(self.val_cache) < (1 << 20):
+                self.val_cache[(idx, d)] = b
+        except TypeError:
+            pass
         return b
 
     def decode(self, idx: int, rec) -> LayerSchedule:
@@ -364,6 +381,8 @@ def candidate_actions(s):
                                     len(prefix), _lib._p(buf), cap, ctypes.byref(n)))
     idx = len(s.decisions)
     out = []
+    if len(inf.enc_cache) >= (1 << 20):
+        inf.enc_cache.clear()
     for r in buf[: n.value]:
         d = inf.decode(idx, r)
         inf.enc_cache[id(d)] = (d, r.tobytes(), idx)
