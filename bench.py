@@ -552,7 +552,9 @@ def main():
             greedy_schedule_gpu(pn, params)  # warm (descriptor upload, prefix)
             t0 = time.perf_counter()
             s, visited = greedy_schedule_gpu(pn, params)
-            greedy[net] = {"wall_s": round(time.perf_counter() - t0, 4), "visited": visited}
+            wall = time.perf_counter() - t0
+            greedy[net] = {"wall_s": round(wall, 4), "visited": visited,
+                           "candidates_per_s": round(visited / wall, 1)}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
