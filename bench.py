@@ -557,7 +557,7 @@ def main():
                            "candidates_per_s": round(visited / wall, 1)}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N=1 only
         try:
             r = cpu_reference(args.cpu_states, repeats=args.cpu_repeats)
             cpu = {"value": r["pool"], "unit": "states/s", "cores": r["cores"], "kind": "reference",
