@@ -1271,8 +1271,8 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
                           ctx->stream));
   TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
-  TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * 4096 + sizeof(Nest)));
-  TS_CUDA(ctx->h_out.reserve(sizeof(double) * 3));
+  TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * (4096 + 8)));
+  TS_CUDA(ctx->h_out.reserve(sizeof(double) * 4));
   uint64_t rng = rng_state ? *rng_state : 0;
   const bool trace = getenv("TS_GREEDY_TRACE") != nullptr;
   double t_enum = 0.0, t_wait = 0.0;
@@ -1293,18 +1293,75 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     if (cnt <= 0) return fail(ctx, cnt < 0 ? (int)-cnt : TS_ERR_PIPELINE, "candidate enumeration");
     const int n = (int)cnt;
     if (n > 4096) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
-    TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * n));
+    TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n + 8)));
     TS_CUDA(ctx->rows.reserve(sizeof(double) * F * n));
-    TS_CUDA(ctx->reps.reserve(sizeof(int) * n));
+    TS_CUDA(ctx->reps.reserve(sizeof(int) * (n + 1)));
     TS_CUDA(ctx->raw.reserve(sizeof(double) * n));
-    TS_CUDA(ctx->out.reserve(sizeof(double) * 2));
-    // stage host data in pinned memory: candidate records + consumer nest
+    TS_CUDA(ctx->out.reserve(sizeof(double) * 3));
+    const bool fused = ctx->hidden == 32;  // H = 32: the 2-kernel layer with the last-block argmin
+    // stage host data in pinned memory: candidate records, then the consumer
+    // nest right behind them (one H2D per layer)
     ts_decision* hs = ctx->h_stage.as<ts_decision>();
     memcpy(hs, cands.data(), sizeof(ts_decision) * n);
-    Nest* hn = reinterpret_cast<Nest*>(hs + 4096);
+    Nest* hn = reinterpret_cast<Nest*>(hs + n);
+    static_assert(sizeof(Nest) <= 8 * sizeof(ts_decision), "nest staging");
     if (cn) *hn = *cn;
-    TS_CUDA(cudaMemcpyAsync(ctx->records.p, hs, sizeof(ts_decision) * n, cudaMemcpyHostToDevice, ctx->stream));
-    if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, hn, sizeof(Nest), cudaMemcpyHostToDevice, ctx->stream));
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, hs, sizeof(ts_decision) * n + (cn ? sizeof(Nest) : 0),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    const Nest* d_nest = reinterpret_cast<const Nest*>(ctx->records.as<ts_decision>() + n);
+    int* ticket = ctx->reps.as<int>() + n;
+    if (fused) {
+      if (!ctx->exact_attr_set) {
+        TS_CUDA(cudaFuncSetAttribute(k_score_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(ExactSmem)));
+        TS_CUDA(cudaFuncSetAttribute(k_children_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(ExactSmem)));
+        ctx->exact_attr_set = true;
+      }
+      k_children_rows_dedup<<<1, 1024, 0, ctx->stream>>>(
+          P->d.as<PipelineDesc>(), s, ctx->records.as<ts_decision>(), n, d_nest, P->init_raw.as<double>(),
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->reps.as<int>(),
+          ctx->status.as<int>(), ticket);
+      TS_LAUNCHED();
+      GreedyTail tail;
+      tail.ticket = ticket;
+      tail.out = ctx->out.as<double>();
+      tail.status = ctx->status.as<int>();
+      tail.state_row = state_rows + (int64_t)s * F;
+      tail.target_scale = ctx->target_scale;
+      tail.eps = epsilon;
+      tail.rng_state0 = rng;
+      const size_t xs_bytes = sizeof(double) * F * (T - s);
+      if (xs_bytes > 48 * 1024)
+        TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)xs_bytes));
+      k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
+                                                             ctx->rows.as<double>(), ctx->reps.as<int>(), n,
+                                                             state_rows, ctx->raw.as<double>(), tail);
+      TS_LAUNCHED();
+      double* ho = ctx->h_out.as<double>();
+      TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+      const double tw0 = trace ? now_us() : 0.0;
+      TS_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (trace) t_wait += now_us() - tw0;
+      const int st = (int)ho[2];
+      if (st) {
+        cudaMemset(ctx->status.p, 0, sizeof(int));
+        return fail(ctx, st, std::string("device: ") + status_name(st));
+      }
+      const int best = (int)ho[1];
+      best_v = ho[0];
+      if (best < 0 || best >= n) return fail(ctx, TS_ERR_CUDA, "argmin produced no index");
+      if (epsilon > 0.0) rng += (uint64_t)n * 0x9E3779B97F4A7C15ull;
+      vis += n;
+      out_decisions[i] = cands[best];
+      int64_t pe[TS_MAX_PURE];
+      const int brc = build_nest(sd, cands[best].anchor >= 0 ? cs : nullptr,
+                                 cands[best].anchor >= 0 ? cn : nullptr, cands[best], nests[s], pe);
+      if (brc) return fail(ctx, brc, status_name(brc));
+      continue;  // the winner's row is already in the state matrix
+    }
+    if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, d_nest, sizeof(Nest), cudaMemcpyDeviceToDevice, ctx->stream));
     k_children_rows<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
         P->d.as<PipelineDesc>(), s, ctx->records.as<ts_decision>(), n, ctx->nest.as<Nest>(),
         P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(),
