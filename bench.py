@@ -202,6 +202,31 @@ def cpu_reference(per_proc: int, seed0: int = 1, single: bool = True, repeats: i
     return out
 
 
+def _ref_cost_worker(args):
+    """The reference's cost_oracle.benchmark on n fresh complete VGG-16
+    schedules (walks untimed)."""
+    seed0, n = args
+    _ref_import()
+    from tensched.cost_oracle import MachineModel, benchmark
+    from tensched.pipeline_ir import parse_pipeline
+    from tensched.schedule_space import apply, candidate_actions, initial_state
+    from tensched.search import SearchRng
+    p = parse_pipeline(VGG.read_text())
+    states = []
+    for seed in range(seed0, seed0 + n):
+        rng = SearchRng(seed)
+        s = initial_state(p)
+        while not s.is_complete:
+            c = candidate_actions(s)
+            s = apply(s, c[rng.randrange(len(c))])
+        states.append(s)
+    m = MachineModel()
+    t0 = time.perf_counter()
+    for s in states:
+        benchmark(s, m)
+    return n / (time.perf_counter() - t0)
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -264,6 +289,12 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     mw = MachineModel().words()
     ctx.check(ctx.lib.ts_benchmark(ctx.h, pid, _lib._p(cd), cd.size, _lib._p(mw), _lib._p(h_recs),
                                    _lib._p(h_offs), S, _lib._p(limbs)))
+    # the device cost oracle (cost_oracle.benchmark) through its
+    # host-buffer C-ABI call, timed on a second pass (descriptor cached)
+    t0 = time.perf_counter()
+    ctx.check(ctx.lib.ts_benchmark(ctx.h, pid, _lib._p(cd), cd.size, _lib._p(mw), _lib._p(h_recs),
+                                   _lib._p(h_offs), S, _lib._p(limbs)))
+    cost_rate = S / (time.perf_counter() - t0)
     millis = [sum(int(limbs[i, k]) << (64 * k) for k in range(4)) for i in range(S)]
     logt_s = np.log(np.array([m / 1000.0 for m in millis]))
     rows = torch.empty((S * T, 16), dtype=torch.float64, device=dev)
@@ -327,6 +358,8 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     # per (sequence, timestep) pair; every sample of this dataset has T timesteps
     wg_flops = 2.0 * 128 * 49 * T * B
     return {"metric": "V-training samples/sec", "value": B * world * K / (ms_tc / 1e3),
+            "cost_oracle": {"value": cost_rate, "unit": "complete VGG-16 schedules/s",
+                            "note": "ts_benchmark (256-bit fixed point, exact), host buffers, per GPU"},
             "unit": "samples/s", "pairs_per_gpu": N, "schedules_per_gpu": S, "batch_per_gpu": B,
             "global_batch": B * world, "steps": K, "ms_per_step": ms_tc / K,
             "mode": "tc: fp64 forward/BPTT, weight gradients on tcgen05 (3xTF32, TMEM, fused into BPTT)",
@@ -570,6 +603,11 @@ def main():
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "states/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
+        if train_line is not None and cpu is not None and cpu.get("value"):
+            try:  # the reference's cost oracle, one process, next to the device one
+                train_line["cost_oracle"]["cpu_reference_1proc"] = _ref_cost_worker((5_000_000, 100))
+            except Exception as e:
+                train_line["cost_oracle"]["cpu_reference_1proc"] = f"unavailable: {e}"
 
     if rank == 0:
         line = {
