@@ -538,17 +538,17 @@ def main():
     if "featurize" in avg and mode == _lib.MODE_FAST:
         # the featurizer's binding resource is instruction issue (integer
         # walk): warp instructions per scheduled row from the ncu capture
-        # (8.879e9 warp instructions for 12.5M states = 218.7M rows),
+        # (9.3225e9 warp instructions for 12.5M states = 218.7M rows),
         # against 4 warp instructions / clk / SM
         mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965
         issue_peak = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * mhz * 1e6
-        issued = 8.879282e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
+        issued = 9.322507e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
         roof["k_featurize_rows_issue"] = {"bound": "issue", "achieved": issued / 1e12, "peak": issue_peak / 1e12,
                                           "unit": "T warp-instr/s", "frac": issued / issue_peak,
-                                          "algorithmic": "40.6 warp instructions per scheduled row (ncu)"}
+                                          "algorithmic": "42.6 warp instructions per scheduled row (ncu)"}
     roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 79%, "
                     "issue 59% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work "
-                    "(ALU 54%, issue 63%); profiles/r01_ncu.md")
+                    "(ALU 58%, issue 67%); profiles/r01_ncu.md")
 
     # ---- batch-size sweep (1e4..1e7 states per GPU), device-resident,
     # on prefixes of this rank's states: where launch latency stops mattering
