@@ -337,6 +337,22 @@ int self_test(ts_ctx* ctx) {
       return fail(ctx, TS_ERR_SELFTEST, buf);
     }
   }
+  // tanh_bf (the branch-free restatement the exact LSTM kernels use) must
+  // equal the device tanh bit for bit
+  DevBuf db;
+  TS_CUDA(db.reserve(16));
+  TS_CUDA(cudaMemset(db.p, 0, 16));
+  k_tanh_selftest<<<296, 256>>>((int64_t)1 << 22, db.as<unsigned long long>());
+  TS_LAUNCHED();
+  unsigned long long hb[2];
+  TS_CUDA(cudaMemcpy(hb, db.p, 16, cudaMemcpyDeviceToHost));
+  if (hb[0]) {
+    char buf[160];
+    double bx;
+    memcpy(&bx, &hb[1], 8);
+    snprintf(buf, sizeof buf, "device tanh_bf mismatch at %.17g (%llu inputs)", bx, hb[0]);
+    return fail(ctx, TS_ERR_SELFTEST, buf);
+  }
   return TS_OK;
 }
 
@@ -1266,8 +1282,11 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   std::vector<ts_decision> cands;
   cands.reserve(1024);
   // device state rows start as the all-unscheduled normalized matrix
-  TS_CUDA(ctx->tmp.reserve(sizeof(double) * T * F));
+  // device state: rows (all-unscheduled normalized matrix to start), then
+  // b + x.Wx per scheduled row (H = 32; written as each winner is installed)
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * T * (F + 128)));
   double* state_rows = ctx->tmp.as<double>();
+  double* zx_state = state_rows + (int64_t)T * F;
   TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
                           ctx->stream));
   TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
@@ -1328,16 +1347,17 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       tail.out = ctx->out.as<double>();
       tail.status = ctx->status.as<int>();
       tail.state_row = state_rows + (int64_t)s * F;
+      tail.zx_row = zx_state + (int64_t)s * 128;
       tail.target_scale = ctx->target_scale;
       tail.eps = epsilon;
       tail.rng_state0 = rng;
-      const size_t xs_bytes = sizeof(double) * F * (T - s);
+      const size_t xs_bytes = exact_mw_smem(T, s, true);
       if (xs_bytes > 48 * 1024)
         TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)xs_bytes));
       k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
                                                              ctx->rows.as<double>(), ctx->reps.as<int>(), n,
-                                                             state_rows, ctx->raw.as<double>(), tail);
+                                                             state_rows, ctx->raw.as<double>(), zx_state, tail);
       TS_LAUNCHED();
       double* ho = ctx->h_out.as<double>();
       TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1378,7 +1398,11 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
                                      (int)sizeof(ExactSmem)));
         ctx->exact_attr_set = true;
       }
-      k_children_exact_mw<<<n, 128, sizeof(double) * F * (T - s), ctx->stream>>>(
+      const size_t xs_bytes = exact_mw_smem(T, s, false);
+      if (xs_bytes > 48 * 1024)
+        TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)xs_bytes));
+      k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(
           lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
                                                       ctx->rows.as<double>(), ctx->reps.as<int>(), n, state_rows,
                                                       ctx->raw.as<double>());
@@ -1500,7 +1524,7 @@ int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, i
   TS_LAUNCHED();
   double* raw = ctx->raw.as<double>();
   if (ctx->hidden == 32) {
-    const size_t xs_bytes = sizeof(double) * F * (T - s);
+    const size_t xs_bytes = exact_mw_smem(T, s, false);
     if (xs_bytes > 48 * 1024)
       TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)xs_bytes));
