@@ -93,6 +93,7 @@ struct PipelineSlot {
 }  // namespace
 
 struct ts_ctx {
+  uint64_t greedy_seq = 0;  // fused greedy: sequence number of the last layer result
   int device = 0;
   cudaStream_t stream = nullptr;       // compute
   cudaStream_t copy_stream = nullptr;  // host->device transfers of ts_score_states*
@@ -1325,11 +1326,13 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     Nest* hn = reinterpret_cast<Nest*>(hs + n);
     static_assert(sizeof(Nest) <= 8 * sizeof(ts_decision), "nest staging");
     if (cn) *hn = *cn;
-    TS_CUDA(cudaMemcpyAsync(ctx->records.p, hs, sizeof(ts_decision) * n + (cn ? sizeof(Nest) : 0),
-                            cudaMemcpyHostToDevice, ctx->stream));
-    const Nest* d_nest = reinterpret_cast<const Nest*>(ctx->records.as<ts_decision>() + n);
     int* ticket = ctx->reps.as<int>() + n;
     if (fused) {
+      // H = 32: the kernels read the candidates and the consumer nest from
+      // the mapped staging buffer (no copy), the exact kernel is a
+      // programmatic dependent of the rows kernel (its weight loads overlap
+      // it), and the last block writes the layer's result into mapped host
+      // memory, which the host polls (no copy, no stream sync)
       if (!ctx->exact_attr_set) {
         TS_CUDA(cudaFuncSetAttribute(k_score_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(ExactSmem)));
@@ -1338,13 +1341,18 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
         ctx->exact_attr_set = true;
       }
       k_children_rows_dedup<<<1, 1024, 0, ctx->stream>>>(
-          P->d.as<PipelineDesc>(), s, ctx->records.as<ts_decision>(), n, d_nest, P->init_raw.as<double>(),
+          P->d.as<PipelineDesc>(), s, hs, n, cn ? hn : nullptr, P->init_raw.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->reps.as<int>(),
           ctx->status.as<int>(), ticket);
       TS_LAUNCHED();
       GreedyTail tail;
       tail.ticket = ticket;
       tail.out = ctx->out.as<double>();
+      volatile double* ho = ctx->h_out.as<double>();
+      const double seq = (double)++ctx->greedy_seq;
+      ho[3] = 0.0;
+      tail.host_out = ho;
+      tail.seq = seq;
       tail.status = ctx->status.as<int>();
       tail.state_row = state_rows + (int64_t)s * F;
       tail.zx_row = zx_state + (int64_t)s * 128;
@@ -1355,14 +1363,34 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       if (xs_bytes > 48 * 1024)
         TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)xs_bytes));
-      k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
-                                                             ctx->rows.as<double>(), ctx->reps.as<int>(), n,
-                                                             state_rows, ctx->raw.as<double>(), zx_state, tail);
+      {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)n);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = xs_bytes;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        TS_CUDA(cudaLaunchKernelEx(&cfg, k_children_exact_mw, lstm_weights(ctx),
+                                   (const double*)P->pre_exact.as<double>(), T, s,
+                                   (const double*)ctx->rows.as<double>(), (const int*)ctx->reps.as<int>(), n,
+                                   (const double*)state_rows, ctx->raw.as<double>(), (const double*)zx_state,
+                                   tail));
+      }
       TS_LAUNCHED();
-      double* ho = ctx->h_out.as<double>();
-      TS_CUDA(cudaMemcpyAsync(ho, ctx->out.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
       const double tw0 = trace ? now_us() : 0.0;
-      TS_CUDA(cudaStreamSynchronize(ctx->stream));
+      // poll the result; every few thousand spins ask the stream whether it
+      // failed or finished without writing one
+      for (uint32_t spin = 1; ho[3] != seq; ++spin) {
+        if ((spin & 4095u) == 0) {
+          const cudaError_t q = cudaStreamQuery(ctx->stream);
+          if (q != cudaSuccess && q != cudaErrorNotReady) TS_CUDA(q);
+          if (q == cudaSuccess && ho[3] != seq) return fail(ctx, TS_ERR_CUDA, "greedy layer wrote no result");
+        }
+      }
       if (trace) t_wait += now_us() - tw0;
       const int st = (int)ho[2];
       if (st) {
@@ -1381,7 +1409,8 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       if (brc) return fail(ctx, brc, status_name(brc));
       continue;  // the winner's row is already in the state matrix
     }
-    if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, d_nest, sizeof(Nest), cudaMemcpyDeviceToDevice, ctx->stream));
+    TS_CUDA(cudaMemcpyAsync(ctx->records.p, hs, sizeof(ts_decision) * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (cn) TS_CUDA(cudaMemcpyAsync(ctx->nest.p, hn, sizeof(Nest), cudaMemcpyHostToDevice, ctx->stream));
     k_children_rows<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
         P->d.as<PipelineDesc>(), s, ctx->records.as<ts_decision>(), n, ctx->nest.as<Nest>(),
         P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(),
