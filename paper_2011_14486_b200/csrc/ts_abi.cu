@@ -291,8 +291,16 @@ int ensure_pipe_ready(ts_ctx* ctx, PipelineSlot* P) {
                                                        ctx->stdv.as<double>(), P->init_raw.as<double>(),
                                                        P->init_norm.as<double>());
   TS_LAUNCHED();
-  k_prefix_exact<<<1, 32, 0, ctx->stream>>>(lstm_weights(ctx), P->init_norm.as<double>(), T,
-                                            ctx->b_out, P->pre_exact.as<double>());
+  const size_t pre_smem = prefix_mw_smem(T);
+  if (ctx->hidden == 32 && pre_smem <= 200 * 1024) {  // the four-warp step (H = 32)
+    if (pre_smem > 40 * 1024)  // with the static 4 KB
+      TS_CUDA(cudaFuncSetAttribute(k_prefix_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pre_smem));
+    k_prefix_exact_mw<<<1, 128, pre_smem, ctx->stream>>>(lstm_weights(ctx), P->init_norm.as<double>(), T,
+                                                         ctx->b_out, P->pre_exact.as<double>());
+  } else {
+    k_prefix_exact<<<1, 32, 0, ctx->stream>>>(lstm_weights(ctx), P->init_norm.as<double>(), T,
+                                              ctx->b_out, P->pre_exact.as<double>());
+  }
   TS_LAUNCHED();
   P->rows_version = ctx->params_version;
   return TS_OK;
@@ -1360,7 +1368,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       tail.eps = epsilon;
       tail.rng_state0 = rng;
       const size_t xs_bytes = exact_mw_smem(T, s, true);
-      if (xs_bytes > 48 * 1024)
+      if (xs_bytes > 40 * 1024)  // with the kernel's static shared memory
         TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)xs_bytes));
       {
@@ -1428,7 +1436,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
         ctx->exact_attr_set = true;
       }
       const size_t xs_bytes = exact_mw_smem(T, s, false);
-      if (xs_bytes > 48 * 1024)
+      if (xs_bytes > 40 * 1024)  // with the kernel's static shared memory
         TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)xs_bytes));
       k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(
@@ -1554,7 +1562,7 @@ int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, i
   double* raw = ctx->raw.as<double>();
   if (ctx->hidden == 32) {
     const size_t xs_bytes = exact_mw_smem(T, s, false);
-    if (xs_bytes > 48 * 1024)
+    if (xs_bytes > 40 * 1024)  // with the kernel's static shared memory
       TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)xs_bytes));
     k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,

@@ -89,3 +89,28 @@ def test_illegal_child_rejected(greedy_golden, v0):
     s1 = ss.child_state(s, acts[0])
     with pytest.raises(PipelineError):
         score_children(v0, s1, acts[:2])  # decisions for the wrong stage
+
+
+def test_children_deep_parent_long_suffix(v0):
+    """ResNet-50 (T = 121) parents one and sixty stages short of complete:
+    the child's suffix LSTM stages up to 121 rows plus its per-step readout
+    in shared memory (past the 48 KB default), and must still equal
+    predict_states on the materialized children bit for bit."""
+    from paper_2011_14486_b200.pipeline_ir import parse_pipeline
+    import pathlib
+    root = pathlib.Path(__file__).resolve().parent.parent
+    p = parse_pipeline((root / "assets/pipelines/nets/resnet50.pl").read_text())
+    T = len(p.stages)
+    s = ss.initial_state(p)
+    parents = {}
+    for i in range(T - 1):
+        acts = ss.candidate_actions(s)
+        s = ss.child_state(s, acts[i % len(acts)])
+        if len(s.decisions) in (60, T - 1):
+            parents[len(s.decisions)] = s
+    for depth, s in parents.items():
+        acts = ss.candidate_actions(s)
+        kids = [ss.child_state(s, a) for a in acts]
+        got = score_children(v0, s, acts)
+        want = predict_states(v0, kids)
+        assert np.array_equal(bits(got), bits(want)), depth
