@@ -124,6 +124,18 @@ def consumers_of(p, name) -> tuple:
     return tuple(s.name for s in p.stages if any(e.producer == name for e in s.inputs))
 
 
+def consumer_map(p) -> dict:
+    """consumers_of for every stage in one pass (name -> consumers in stage order)."""
+    out = {s.name: [] for s in p.stages}
+    for s in p.stages:
+        seen = set()
+        for e in s.inputs:
+            if e.producer in out and e.producer not in seen:
+                seen.add(e.producer)
+                out[e.producer].append(s.name)
+    return {k: tuple(v) for k, v in out.items()}
+
+
 # ------------------------------------------------------------- text format
 def _dim_list(text, lineno):
     out = []
@@ -277,8 +289,9 @@ def descriptor(p) -> np.ndarray:
     pos = {n: i for i, n in enumerate(topo)}
     st = _stage_index(p)
     sole = {}
+    cmap = consumer_map(p)
     for n in topo:
-        cons = consumers_of(p, n)
+        cons = cmap[n]
         sole[n] = cons[0] if len(cons) == 1 else None
     # slot allocation over schedule indices (sched(s) = T-1-pos(s))
     live_end = {}

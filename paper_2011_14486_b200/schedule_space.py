@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .errors import IllegalActionError, PipelineError
-from .pipeline_ir import consumers_of, descriptor, schedule_order, topological_order
+from .pipeline_ir import consumer_map, consumers_of, descriptor, schedule_order, topological_order
 
 SPLIT_FACTORS = (8, 32)  # schedule_space.py:28-30
 VEC_WIDTHS = (1, 8)
@@ -123,8 +123,9 @@ class _PipelineInfo:
         self.stages = [by_name[n] for n in self.sched]
         self.sole = []
         self.loop_ids = []    # per schedule index: (split-set) -> {loop name: id}
+        cmap = consumer_map(p)
         for st in self.stages:
-            cons = consumers_of(p, st.name)
+            cons = cmap[st.name]
             self.sole.append(cons[0] if len(cons) == 1 else None)
         self.enc_cache = {}   # id(decision) -> (decision, bytes, schedule index)
         # (schedule index, decision) -> bytes: decisions are frozen dataclasses,
