@@ -187,7 +187,10 @@ int ts_check_action(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int
 /* Fused greedy_schedule: returns the n_stages decisions and the visited
  * candidate count.  epsilon > 0 applies the multiplicative noise of
  * search.py:104-109 from the splitmix64 stream *rng_state (advanced by one
- * draw per candidate, exactly as SearchRng). */
+ * draw per candidate, exactly as SearchRng).  With H = 32 the calling
+ * thread polls each layer's result in mapped pinned memory (a busy wait,
+ * like a spinning stream sync) and checks the stream for errors while it
+ * waits; the call returns with the context's stream idle. */
 int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
               ts_decision* out_decisions, int64_t* visited, double* out_best_v);
 
