@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <atomic>
 #include <memory>
 #include <string>
 #include <vector>
@@ -50,6 +51,17 @@ struct DevBuf {
     cudaError_t e = cudaMalloc(&p, n);
     if (e == cudaSuccess) bytes = n;
     return e;
+  }
+  // Growth of a buffer that kernels queued on `user` may still read: wait
+  // for that stream before the old allocation is released (explicitly, not
+  // through cudaFree's implicit device synchronization).
+  cudaError_t reserve(size_t n, cudaStream_t user) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) {
+      cudaError_t e = cudaStreamSynchronize(user);
+      if (e != cudaSuccess) return e;
+    }
+    return reserve(n);
   }
   template <typename T>
   T* as() const {
@@ -658,6 +670,11 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   return TS_OK;
 }
 
+// FAST scratch of a batch: rowoff[T + 2] (int64), perm[n], hist/cursor[T + 2]
+static size_t fast_reps_bytes(int T, int64_t n_states) {
+  return sizeof(int64_t) * (T + 2) + sizeof(int) * (n_states + 2 * (T + 2));
+}
+
 // d_codes (optional): 16-bit action codes instead of records, same offsets
 static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_records,
                         const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
@@ -666,7 +683,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
   if (rc) return rc;
   const int T = P->h->n_stages;
   if (mode == TS_MODE_EXACT) {
-    TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1)));
+    TS_CUDA(ctx->rows.reserve(sizeof(double) * F * (n_records > 0 ? n_records : 1), ctx->stream));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
@@ -704,7 +721,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     rc = ensure_fast_prefix(ctx, P);
     if (rc) return rc;
     // bucket states by depth (descending) so tiles share their depth
-    TS_CUDA(ctx->reps.reserve(sizeof(int64_t) * (T + 2) + sizeof(int) * (n_states + 2 * (T + 2))));
+    TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, n_states), ctx->stream));
     int64_t* rowoff = ctx->reps.as<int64_t>();
     int* perm = reinterpret_cast<int*>(rowoff + (T + 2));
     int* hist = perm + n_states;
@@ -723,7 +740,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
                             sizeof(int) * 2 * (T + 1), ctx->stream>>>(d_offsets, n_states, T, cursor, perm);
       TS_LAUNCHED();
     }
-    TS_CUDA(ctx->rows.reserve(sizeof(float) * 8 * (n_records > 0 ? n_records : 1)));
+    TS_CUDA(ctx->rows.reserve(sizeof(float) * 8 * (n_records > 0 ? n_records : 1), ctx->stream));
     {
       KTimer kt(ctx, TS_K_FEATURIZE);
       k_featurize_rows<float><<<(unsigned)((n_states + TS_FEAT_BLOCK - 1) / TS_FEAT_BLOCK), TS_FEAT_BLOCK,
@@ -748,7 +765,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     ta.record_prefix = 0;
     ta.target_scale = ctx->target_scale;
     ta.b_out = ctx->b_out;
-    TS_CUDA(ctx->tile_ctr.reserve(sizeof(int)));
+    TS_CUDA(ctx->tile_ctr.reserve(sizeof(int), ctx->stream));
     TS_CUDA(cudaMemsetAsync(ctx->tile_ctr.p, 0, sizeof(int), ctx->stream));
     ta.tile_counter = ctx->tile_ctr.as<int>();
     {
@@ -1027,9 +1044,40 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     TS_LAUNCHED();
   }
   std::vector<cudaEvent_t> ev;
+  // every exit (errors included) waits for all four streams before the
+  // caller's buffers are released, and returns the events to the pool
+  struct Drain {
+    ts_ctx* c;
+    std::vector<cudaEvent_t>& ev;
+    ~Drain() {
+      cudaStreamSynchronize(c->copy_stream);
+      cudaStreamSynchronize(c->stream);
+      if (c->stream2) cudaStreamSynchronize(c->stream2);
+      cudaStreamSynchronize(c->d2h_stream);
+      for (auto e : ev) c->event_pool.push_back(e);
+      ev.clear();
+    }
+  } drain{ctx, ev};
   // FAST: chunks alternate between two lanes (the exact leg indexes its rows
   // by global record offsets, so it stays on one lane)
   const bool two_lanes = mode == TS_MODE_FAST && n_chunks > 1 && !getenv("TS_ONE_LANE");
+  {  // per-lane scratch sized for the largest chunk up front, so no buffer a
+     // queued kernel reads is reallocated while chunks are in flight
+    int64_t max_chunk = 0;
+    for (int64_t k = 0; k < n_chunks; ++k) max_chunk = std::max(max_chunk, st_at[k + 1] - st_at[k]);
+    size_t temp = 0;
+    TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, d_off + 1, d_off + 1, max_chunk, ctx->stream));
+    const size_t rows_bound = sizeof(float) * 8 * (size_t)max_chunk * T;  // depth <= T
+    if (two_lanes && !ctx->stream2) TS_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    for (int ln = 0; ln < (two_lanes ? 2 : 1); ++ln) {
+      LaneSwap lane(ctx, ln == 1);
+      TS_CUDA(ctx->scan_tmp.reserve(temp + 16, ctx->stream));
+      if (mode == TS_MODE_FAST) {
+        TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, max_chunk), ctx->stream));
+        if (rows_bound <= ((size_t)2 << 30)) TS_CUDA(ctx->rows.reserve(rows_bound, ctx->stream));
+      }
+    }
+  }
   if (two_lanes) {
     if (!ctx->stream2) TS_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
     cudaEvent_t setup = take_event(ctx);  // code table, prefix: issued on lane 0
@@ -1042,11 +1090,8 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     const int64_t s0 = st_at[k], s1 = st_at[k + 1];
     LaneSwap lane(ctx, two_lanes && (k & 1));
     const int64_t r0 = n_rec, r1 = r0 + (int64_t)sum_bytes(depths + s0, s1 - s0);
-    if (r1 > rec_cap || (r1 > r0 && !codes)) {
-      cudaStreamSynchronize(ctx->copy_stream);  // no copy may outlive the caller's buffers
-      cudaStreamSynchronize(ctx->stream);
+    if (r1 > rec_cap || (r1 > r0 && !codes))  // (Drain: no copy outlives the caller's buffers)
       return fail(ctx, TS_ERR_ARG, r1 > rec_cap ? "state depth exceeds the pipeline's stage count" : "no codes");
-    }
     n_rec = r1;
     TS_CUDA(cudaMemcpyAsync(d_depth + s0, depths + s0, s1 - s0, cudaMemcpyHostToDevice, ctx->copy_stream));
     if (r1 > r0)
@@ -1063,7 +1108,7 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     TS_LAUNCHED();
     size_t temp = 0;
     TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
-    TS_CUDA(ctx->scan_tmp.reserve(temp + 16));
+    TS_CUDA(ctx->scan_tmp.reserve(temp + 16, ctx->stream));
     TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
     ++ctx->launches;
     // FAST rows are chunk-local (decision-major by rowoff); the exact leg's
@@ -1080,7 +1125,6 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
   }
   TS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   TS_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
-  for (auto e : ev) ctx->event_pool.push_back(e);
   return check_device_status(ctx);
 }
 
@@ -1400,6 +1444,10 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
         }
       }
       if (trace) t_wait += now_us() - tw0;
+      // the device wrote {v, index, status} before seq (__threadfence_system);
+      // order the host's reads of them after its read of seq (not implied on
+      // weakly ordered hosts such as aarch64)
+      std::atomic_thread_fence(std::memory_order_acquire);
       const int st = (int)ho[2];
       if (st) {
         cudaMemset(ctx->status.p, 0, sizeof(int));

@@ -75,23 +75,23 @@ def featurize_states(states, cache_size=None, params=None, normalized=False, dev
     if cache_size not in (None, DEFAULT_CACHE_SIZE):
         raise PipelineError("only the default cache size (32768) is featurized on device")
     ctx = _lib.context(device)
-    if params is None:
-        if normalized:
-            raise PipelineError("normalized features need params")
-        if ctx._params_key is None:
-            ctx.set_params(_identity_params())
-    else:
-        ctx.set_params(params)
     out = [None] * len(states)
-    for inf, idxs, recs, offsets in encode_states(states):
-        pid = ctx.pipeline_id(inf.desc)
-        buf = np.empty((len(idxs), inf.T, FEATURE_WIDTH), dtype=np.float64)
-        with ctx.lock:
+    with ctx.lock:  # params upload and the calls that normalize with them
+        if params is None:
+            if normalized:
+                raise PipelineError("normalized features need params")
+            if ctx._params_key is None:
+                ctx.set_params(_identity_params())
+        else:
+            ctx.set_params(params)
+        for inf, idxs, recs, offsets in encode_states(states):
+            pid = ctx.pipeline_id(inf.desc)
+            buf = np.empty((len(idxs), inf.T, FEATURE_WIDTH), dtype=np.float64)
             ctx.check(ctx.lib.ts_featurize_states(
                 ctx.h, pid, _lib._p(recs) if len(recs) else None, _lib._p(offsets), len(idxs),
                 1 if normalized else 0, _lib._p(buf)))
-        for j, i in enumerate(idxs):
-            out[i] = buf[j]
+            for j, i in enumerate(idxs):
+                out[i] = buf[j]
     return out
 
 

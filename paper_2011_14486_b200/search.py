@@ -93,15 +93,15 @@ def score_children(params, s, actions, noise: NoiseConfig | None = None, rng: Se
         raise PipelineError("noisy evaluation needs an rng")
     inf = _info(s.pipeline)
     ctx = _lib.context(device)
-    ctx.set_params(params)
-    pid = ctx.pipeline_id(inf.desc)
     parent = np.frombuffer(inf.records_of(s), dtype=_lib.DECISION_DTYPE)
     pos = len(s.decisions)
     kids = np.frombuffer(b"".join(inf.encode(pos, a) for a in actions), dtype=_lib.DECISION_DTYPE)
     st = ctypes.c_uint64(rng.state if rng is not None else 0)
     if best:
         bi, bv = ctypes.c_int64(), ctypes.c_double()
-        with ctx.lock:
+        with ctx.lock:  # params upload and the call that scores with them
+            ctx.set_params(params)
+            pid = ctx.pipeline_id(inf.desc)
             ctx.check(ctx.lib.ts_score_children(ctx.h, pid, _lib._p(parent) if len(parent) else None,
                                                 len(parent), _lib._p(kids), len(kids), eps, ctypes.byref(st),
                                                 None, ctypes.byref(bi), ctypes.byref(bv)))
@@ -110,6 +110,8 @@ def score_children(params, s, actions, noise: NoiseConfig | None = None, rng: Se
         return bi.value, bv.value
     out = np.empty(len(kids))
     with ctx.lock:
+        ctx.set_params(params)
+        pid = ctx.pipeline_id(inf.desc)
         ctx.check(ctx.lib.ts_score_children(ctx.h, pid, _lib._p(parent) if len(parent) else None,
                                             len(parent), _lib._p(kids), len(kids), 0.0, None,
                                             _lib._p(out), None, None))
@@ -148,14 +150,14 @@ def greedy_schedule_gpu(p, params, noise: NoiseConfig | None = None,
     if eps > 0 and rng is None:
         raise PipelineError("noisy evaluation needs an rng")
     ctx = _lib.context(device)
-    ctx.set_params(params)
     inf = _info(p)
-    pid = ctx.pipeline_id(inf.desc)
     out = np.zeros(inf.T, dtype=_lib.DECISION_DTYPE)
     visited = ctypes.c_int64()
     best_v = ctypes.c_double()
     st = ctypes.c_uint64(rng.state if rng is not None else 0)
-    with ctx.lock:
+    with ctx.lock:  # params upload and the greedy that scores with them
+        ctx.set_params(params)
+        pid = ctx.pipeline_id(inf.desc)
         ctx.check(ctx.lib.ts_greedy(ctx.h, pid, eps, ctypes.byref(st), _lib._p(out),
                                     ctypes.byref(visited), ctypes.byref(best_v)))
     if rng is not None and eps > 0:

@@ -76,14 +76,16 @@ def predict_states(params, states, jobs: int = 1, mode: int = MODE_EXACT, device
     if not states:
         return out
     ctx = _lib.context(device)
-    ctx.set_params(params)
-    for inf, idxs, recs, offsets in encode_states(states):
-        pid = ctx.pipeline_id(inf.desc)
-        vals = np.empty(len(idxs))
-        big = len(idxs) >= PACKED_MIN and inf.T < 256
-        codes = action_codes(inf, recs, offsets) if big else None
-        packed = _lib.pack_records(recs) if big and codes is None else None
-        with ctx.lock:
+    # one critical section from the parameter upload to the last scoring
+    # call: a thread sharing the context with other params cannot interleave
+    with ctx.lock:
+        ctx.set_params(params)
+        for inf, idxs, recs, offsets in encode_states(states):
+            pid = ctx.pipeline_id(inf.desc)
+            vals = np.empty(len(idxs))
+            big = len(idxs) >= PACKED_MIN and inf.T < 256
+            codes = action_codes(inf, recs, offsets) if big else None
+            packed = _lib.pack_records(recs) if big and codes is None else None
             if codes is not None:  # 2 bytes per decision (ts_score_states_coded)
                 depths = np.diff(offsets).astype(np.uint8)
                 ctx.check(ctx.lib.ts_score_states_coded(ctx.h, pid, _lib._p(codes), _lib._p(depths),
@@ -96,7 +98,7 @@ def predict_states(params, states, jobs: int = 1, mode: int = MODE_EXACT, device
                 ctx.check(ctx.lib.ts_score_states(ctx.h, pid, _lib._p(recs) if len(recs) else None,
                                                   _lib._p(offsets), len(idxs), int(mode),
                                                   _lib._p(vals)))
-        out[np.asarray(idxs)] = vals
+            out[np.asarray(idxs)] = vals
     return out
 
 

@@ -151,3 +151,11 @@ def test_deep_compute_at_levels(v0_path):
     np.testing.assert_allclose(predict_states(params, states), want, rtol=1e-12)
     np.testing.assert_allclose(predict_states(params, states * 2000, mode=MODE_FAST), np.tile(want, 2000),
                                rtol=1e-4)
+
+
+def test_round_config_rejects_zero_schedules():
+    """learner.RoundConfig validates like the reference (learner.py:131-133)."""
+    from paper_2011_14486_b200.learner import RoundConfig
+    with pytest.raises(PipelineError):
+        RoundConfig(schedules_per_pipeline=0)
+    assert RoundConfig(schedules_per_pipeline=1).schedules_per_pipeline == 1
