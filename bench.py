@@ -44,6 +44,8 @@ VGG = ROOT / "assets" / "pipelines" / "nets" / "vgg16.pl"
 FLOPS_PER_STEP = 12352  # 2*48*128 MMA + 64 readout flops per state-timestep
 RECORD_BYTES = 16
 ROW_BYTES = 128
+TRAFFIC_SOURCE = ("constant: dram__bytes_read.sum + dram__bytes_write.sum per state from one ncu --set full "
+                  "capture at 12.5M states (profiles/), scaled to this launch; not measured in this run")
 
 
 def parse_args():
@@ -63,6 +65,11 @@ def parse_args():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-pairs", type=int, default=10_000_000, help="training pairs per GPU")
     ap.add_argument("--train-batch", type=int, default=4096, help="per-GPU minibatch")
+    ap.add_argument("--big-states", type=int, default=100_000_000,
+                    help="single-GPU sweep point (configs[3]'s 1e8 states on one GPU; 0 = skip)")
+    ap.add_argument("--no-ref-greedy", action="store_true",
+                    help="skip timing the reference's greedy_schedule on this host")
+    ap.add_argument("--no-exact", action="store_true", help="skip the fp64 leg's sweep rate")
     return ap.parse_args()
 
 
@@ -227,6 +234,31 @@ def _ref_cost_worker(args):
     return n / (time.perf_counter() - t0)
 
 
+def _ref_greedy_worker(net):
+    """The reference's own greedy_schedule with its model_value V-callable
+    (cli.py:cmd_schedule's timed region, cli.py:226-232) on one benchmark
+    network, v0.ckpt: wall time, visited count and the schedule."""
+    _ref_import()
+    from tensched.pipeline_ir import parse_pipeline
+    from tensched.search import greedy_schedule, model_value
+    from tensched.value_model import load
+    params = load(str(GOLD / "v0.ckpt"))
+    p = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
+    V = model_value(params)
+    t0 = time.perf_counter()
+    s, visited = greedy_schedule(p, V)
+    wall = time.perf_counter() - t0
+    return net, wall, visited, [d.render() for d in s.decisions]
+
+
+def reference_greedy(nets):
+    """One process per network (they run side by side on the host's cores;
+    each wall time is its own process's)."""
+    import multiprocessing as mp
+    with mp.get_context("spawn").Pool(len(nets)) as pool:
+        return {r[0]: r[1:] for r in pool.map(_ref_greedy_worker, nets)}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -261,14 +293,18 @@ def run_reference_arm(args):
 
 # --------------------------------------------------------------- V training
 def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
-    """BASELINE configs[4]: V training on (partial schedule, simulated cost)
-    pairs over VGG-16, data parallel.  Per rank (untimed): complete random
+    """BASELINE configs[4]: V training on 10M (partial schedule, simulated
+    cost) pairs over VGG-16, data parallel - the pairs are sharded across
+    ranks (each rank holds 10M / world).  Per rank (untimed): complete random
     schedules on the device (search.random_schedule walk), their simulated
     costs from the device cost oracle (cost_oracle.benchmark), and every
     prefix of each schedule as a pair (learner.bootstrap without the
-    cross-schedule min-aggregation), rows featurized once per schedule.
-    Timed: K SGD steps of a per-rank minibatch - gradients on the device,
-    NCCL all-reduce of the 6,305-double gradient, clip + update."""
+    cross-schedule min-aggregation), rows featurized once per schedule;
+    65,536 pairs per rank are held out.  Timed: ONE EPOCH over the training
+    pairs (a fresh permutation, global minibatch = per-rank batch x world) -
+    gradients on the device, NCCL all-reduce of the 6,305-double gradient
+    (N > 1), clip + SGD update - once per gradient mode.  Fit quality: the
+    holdout MSE of log cost (value_model.loss) before and after the epoch."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -276,7 +312,8 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     from paper_2011_14486_b200.cost_oracle import MachineModel, cost_descriptor
     from paper_2011_14486_b200.trainer import DeviceGradients, flat_params
     T = inf.T
-    S = max(1, args.train_pairs // (T + 1))
+    S_total = max(world, args.train_pairs // (T + 1))
+    S = S_total // world
     seed0 = 10_000_000 + rank * S
     recs = torch.empty(S * T * 16, dtype=torch.uint8, device=dev)
     ctx.check(ctx.lib.ts_generate_schedules_device(ctx.h, pid, seed0, 1, S, recs.data_ptr()))
@@ -309,67 +346,177 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     init_base = torch.zeros(N, dtype=torch.int32, device=dev)
     Tl = torch.full((N,), T, dtype=torch.int32, device=dev)
     logt = torch.from_numpy(logt_s).to(dev)[sched]
+    logt_h = logt.cpu().numpy()
     g = DeviceGradients.from_device(ctx, rows.data_ptr(), S * T, init.data_ptr(), T, row_base.data_ptr(),
                                     init_base.data_ptr(), Tl.data_ptr(), depth.data_ptr(),
                                     logt.data_ptr(), N, params.hidden)
-    g.set_params(flat_params(params))
     B = args.train_batch
     rng = np.random.Generator(np.random.PCG64(1234 + rank))
+    perm = rng.permutation(N).astype(np.int32)
+    n_hold = min(65536, N // 10)
+    hold, train_idx = perm[:n_hold], perm[n_hold:]
+    # value_model.train's target scale: the mean log target of the training split
+    tsum = torch.tensor([float(logt_h[train_idx].sum()), float(len(train_idx))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tsum)
+    target_scale = float(tsum[0].item() / tsum[1].item())
     gbuf = torch.zeros(g.n_params, dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(ctx.lib.ts_stream(ctx.h), device=dev)
+    steps = len(train_idx) // B  # one epoch (every rank takes the same number of steps)
+    if world > 1:
+        st = torch.tensor([steps], dtype=torch.int64, device=dev)
+        dist.all_reduce(st, op=dist.ReduceOp.MIN)
+        steps = int(st.item())
+    lr, clip = 1e-2, 5.0  # TrainConfig defaults (value_model.py:74-88)
 
-    def step():
-        idx = rng.integers(0, N, size=B).astype(np.int32)
-        g.grads(idx, B * world, params.target_scale, gbuf.data_ptr())
+    def holdout_mse():
+        raw = np.concatenate([g.forward(hold[k:k + 16384]) for k in range(0, len(hold), 16384)])
+        e = raw + target_scale - logt_h[hold]
+        acc = torch.tensor([float(e @ e), float(len(e))], dtype=torch.float64, device=dev)
         if world > 1:
-            g.sync()
-            dist.all_reduce(gbuf)
-            torch.cuda.synchronize(dev)
-        g.apply(1e-3, 5.0, gbuf.data_ptr())
+            dist.all_reduce(acc)
+        return float(acc[0].item() / acc[1].item())
 
-    K = max(5, args.steps * 2)
+    def epoch(order, n_steps):
+        for k in range(n_steps):
+            idx = order[k * B:(k + 1) * B]
+            g.grads(idx, B * world, target_scale, gbuf.data_ptr())
+            if world > 1:
+                g.sync()
+                dist.all_reduce(gbuf)
+                torch.cuda.synchronize(dev)
+            g.apply(lr, clip, gbuf.data_ptr())
+
     p0 = flat_params(params)
 
     def timed(mode):
         g.set_mode(mode)
         g.set_params(p0)
-        for _ in range(3):
-            step()
+        before = holdout_mse()
+        order = train_idx[rng.permutation(len(train_idx))]
+        epoch(order, 3)  # warm-up steps, then back to p0
+        g.set_params(p0)
         g.sync()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(K):
-            step()
+        epoch(order, steps)
         e1.record(stream)
         g.sync()
         ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        final = g.get_params()
-        assert np.all(np.isfinite(final))
-        return float(ms.item())
+        assert np.all(np.isfinite(g.get_params()))
+        after = holdout_mse()
+        return float(ms.item()), before, after
 
-    ms_exact = timed("exact")
-    ms_tc = timed("tc")
+    ms_exact, b_ex, a_ex = timed("exact")
+    ms_tc, b_tc, a_tc = timed("tc")
     g.set_mode("exact")
+    samples = B * world * steps
     # algorithmic weight-gradient flops of one step: 2 * 128 x 49 ([x | h_prev | 1])
     # per (sequence, timestep) pair; every sample of this dataset has T timesteps
     wg_flops = 2.0 * 128 * 49 * T * B
-    return {"metric": "V-training samples/sec", "value": B * world * K / (ms_tc / 1e3),
+    return {"metric": "V-training samples/sec", "value": samples / (ms_tc / 1e3),
             "cost_oracle": {"value": cost_rate, "unit": "complete VGG-16 schedules/s",
                             "note": "ts_benchmark (256-bit fixed point, exact), host buffers, per GPU"},
-            "unit": "samples/s", "pairs_per_gpu": N, "schedules_per_gpu": S, "batch_per_gpu": B,
-            "global_batch": B * world, "steps": K, "ms_per_step": ms_tc / K,
+            "unit": "samples/s", "pairs_total": S * world * (T + 1), "pairs_per_gpu": N,
+            "holdout_pairs_per_gpu": int(n_hold), "schedules_per_gpu": S, "batch_per_gpu": B,
+            "global_batch": B * world, "steps": steps, "timed": "one epoch over the training pairs",
+            "ms_per_step": ms_tc / steps, "lr": lr, "clip_norm": clip,
             "mode": "tc: fp64 forward/BPTT, weight gradients on tcgen05 (3xTF32, TMEM, fused into BPTT)",
             "dtype": "f64 recurrences + tf32x3 weight-gradient GEMM",
             "weight_grad_tflops_per_step": wg_flops / 1e12,
-            "exact": {"value": B * world * K / (ms_exact / 1e3), "ms_per_step": ms_exact / K,
-                      "dtype": "f64", "note": "fp64 throughout: the reference's trajectory"},
+            "holdout_mse_log": {"before": b_tc, "after_epoch": a_tc},
+            "exact": {"value": samples / (ms_exact / 1e3), "ms_per_step": ms_exact / steps,
+                      "dtype": "f64", "holdout_mse_log": {"before": b_ex, "after_epoch": a_ex},
+                      "note": "fp64 throughout: the reference's trajectory"},
             "parallelism": f"dp{world}", "collective": "NCCL all_reduce(sum) of the gradient"
                                                        if world > 1 else "none",
             "targets": "device cost oracle (cost_oracle.benchmark) of each prefix's schedule"}
+
+
+# --------------------------------------------------------------- 1e8 states, one GPU
+def big_sweep(ctx, pid, T, n_big, shard, mode, dev, stream, ref_out):
+    """BASELINE configs[3]'s largest point on ONE GPU: n_big random partial
+    VGG-16 schedules (seeds 1..n_big, the same walk as the main sweep),
+    generated shard by shard on the device and kept as 16-bit action codes
+    (2 B per decision).  `device`: scored device-resident, shard-sized calls
+    over the one HBM-resident code array (absolute offsets).  `e2e`: the whole
+    1e8 states in ONE ts_score_states_coded call from pinned host buffers
+    (H2D of codes + depths and D2H of V inside the timed region)."""
+    import numpy as np
+    import torch
+    from paper_2011_14486_b200 import _lib
+    n_sh = -(-n_big // shard)
+    recs = torch.empty(shard * T * 16, dtype=torch.uint8, device=dev)
+    offs = torch.empty(shard + 1, dtype=torch.int64, device=dev)
+    codes, depths = [], []
+    t_gen = time.perf_counter()
+    for k in range(n_sh):
+        m = min(shard, n_big - k * shard)
+        nrec = ctypes.c_int64()
+        ctx.check(ctx.lib.ts_generate_states_device(ctx.h, pid, 1 + k * shard, m, recs.data_ptr(),
+                                                    offs.data_ptr(), ctypes.byref(nrec)))
+        c = torch.empty(max(nrec.value, 1), dtype=torch.int16, device=dev)
+        ctx.check(ctx.lib.ts_encode_codes_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), m, c.data_ptr()))
+        codes.append(c[: nrec.value])
+        depths.append((offs[1: m + 1] - offs[:m]).to(torch.uint8))
+    del recs, offs
+    d_codes = torch.cat(codes)
+    del codes
+    d_depth = torch.cat(depths)
+    del depths
+    d_offs = torch.zeros(n_big + 1, dtype=torch.int64, device=dev)
+    d_offs[1:] = torch.cumsum(d_depth.to(torch.int64), 0)
+    n_rec = int(d_offs[-1].item())
+    t_gen = time.perf_counter() - t_gen
+    d_out = torch.empty(n_big, dtype=torch.float64, device=dev)
+    bounds = [(k * shard, min(n_big, (k + 1) * shard)) for k in range(n_sh)]
+    h_off = d_offs.cpu().numpy()
+
+    def dev_step():
+        for s0, s1 in bounds:
+            r = int(h_off[s1] - h_off[s0]) if mode == _lib.MODE_FAST else n_rec
+            ctx.check(ctx.lib.ts_score_states_coded_device(
+                ctx.h, pid, d_codes.data_ptr(), d_offs.data_ptr() + 8 * s0, s1 - s0, r, mode,
+                d_out.data_ptr() + 8 * s0))
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps
+
+    ms_dev = timed(dev_step, 2)
+    h_codes = torch.empty(n_rec, dtype=torch.int16, pin_memory=True)
+    h_codes.copy_(d_codes)
+    h_depth = torch.empty(n_big, dtype=torch.uint8, pin_memory=True)
+    h_depth.copy_(d_depth)
+    h_out = torch.empty(n_big, dtype=torch.float64, pin_memory=True)
+    del d_codes, d_depth
+
+    def e2e_step():
+        ctx.check(ctx.lib.ts_score_states_coded(ctx.h, pid, h_codes.data_ptr(), h_depth.data_ptr(), n_big, mode,
+                                                h_out.data_ptr()))
+    ms_e2e = timed(e2e_step, 2)
+    v_dev = d_out.cpu().numpy()
+    assert np.array_equal(h_out.numpy(), v_dev), "1e8 point: e2e and device-resident V differ"
+    m0 = min(len(ref_out), n_big)
+    assert np.array_equal(v_dev[:m0], ref_out[:m0]), "1e8 point: first shard differs from the main sweep"
+    assert np.all(np.isfinite(v_dev)) and np.all(v_dev > 0)
+    return {"states": n_big, "records": n_rec, "value": n_big / (ms_dev / 1e3), "ms": ms_dev,
+            "e2e": {"value": n_big / (ms_e2e / 1e3), "ms": ms_e2e, "h2d_bytes": 2 * n_rec + n_big,
+                    "d2h_bytes": 8 * n_big, "call": "one ts_score_states_coded call, pinned host buffers"},
+            "unit": "states/s", "generate_s": round(t_gen, 1),
+            "note": f"{n_sh} shard-sized device-resident calls over one HBM-resident code array; the "
+                    "first shard's V equals the main sweep's bit for bit"}
 
 
 # --------------------------------------------------------------- GPU arm
@@ -492,6 +639,33 @@ def main():
     e2e_value = total_states / (float(t2.item()) / 1e3)
     assert np.allclose(h_out.numpy(), out.cpu().numpy(), rtol=0, atol=0)
 
+    # ---- the exact fp64 leg on the same states (device-resident; the
+    # precision the reference computes in, what the greedy parity uses)
+    exact_leg = None
+    if mode == _lib.MODE_FAST and not args.no_exact:
+        out_ex = torch.empty(M, dtype=torch.float64, device=dev)
+
+        def ex_step():
+            ctx.check(ctx.lib.ts_score_states_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M,
+                                                     n_records, _lib.MODE_EXACT, out_ex.data_ptr()))
+        ex_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(2):
+            ex_step()
+        e1.record(stream)
+        barrier()
+        tx = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tx, op=dist.ReduceOp.MAX)
+        rel = (out / out_ex - 1).abs().max().item()
+        exact_leg = {"value": 2 * M * world / (float(tx.item()) / 1e3), "unit": "states/s", "dtype": "f64",
+                     "ms_per_step": float(tx.item()) / 2, "steps": 2,
+                     "fast_vs_exact_max_rel": rel,
+                     "note": "same states, device-resident; fp64 in the Cython kernel's operation order"}
+        del out_ex
+
     # ---- roofline of the dominant kernel
     offs_h = h_offs.numpy()
     depths = np.diff(offs_h)
@@ -513,6 +687,7 @@ def main():
         roof = {"kernel": "k_featurize_rows", "bound": "hbm", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
                 "traffic": tr * M if tr and mode == _lib.MODE_FAST else None,
+                "traffic_source": TRAFFIC_SOURCE,
                 "bytes_per_launch": bytes_per_launch,
                 "algorithmic": f"16 B record read + {row_bytes} B row written per scheduled stage"}
     else:
@@ -522,7 +697,8 @@ def main():
         tr = traffic_per_state.get(dom)
         roof = {"kernel": "k_lstm_tc" if dom == "lstm_fast" else "k_score_exact", "bound": "tensor",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": tr * M if tr else None, "flops_per_launch": flops_per_launch,
+                "traffic": tr * M if tr else None, "traffic_source": TRAFFIC_SOURCE,
+                "flops_per_launch": flops_per_launch,
                 "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
     roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
     if "lstm_fast" in avg:
@@ -545,7 +721,10 @@ def main():
         issued = 9.322507e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
         roof["k_featurize_rows_issue"] = {"bound": "issue", "achieved": issued / 1e12, "peak": issue_peak / 1e12,
                                           "unit": "T warp-instr/s", "frac": issued / issue_peak,
-                                          "algorithmic": "42.6 warp instructions per scheduled row (ncu)"}
+                                          "algorithmic": "42.6 warp instructions per scheduled row (ncu)",
+                                          "instructions_source": "constant from one ncu --set full "
+                                                                 "capture (profiles/r01_ncu.md), not "
+                                                                 "measured in this run"}
     roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 79%, "
                     "issue 59% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work "
                     "(ALU 58%, issue 67%); profiles/r01_ncu.md")
@@ -573,6 +752,13 @@ def main():
         torch.cuda.synchronize(dev)
         sweep[f"{n_sw:.0e}"] = round(n_sw * reps / (e0.elapsed_time(e1) / 1e3), 1)
 
+    big = None
+    if args.big_states and world == 1 and args.big_states > M:
+        vals_main = out.cpu().numpy()
+        big = big_sweep(ctx, pid, T, args.big_states, M, mode, dev, stream, vals_main)
+        sweep[f"{args.big_states:.0e}"] = round(big["value"], 1)
+        torch.cuda.empty_cache()
+
     train_line = None
     if not args.no_train:
         train_line = train_throughput(ctx, pid, inf, params, rank, world, dev, args)
@@ -588,8 +774,28 @@ def main():
             t0 = time.perf_counter()
             s, visited = greedy_schedule_gpu(pn, params)
             wall = time.perf_counter() - t0
+            vis, distinct = ctypes.c_int64(), ctypes.c_int64()
+            ctx.check(ctx.lib.ts_greedy_stats(ctx.h, ctypes.byref(vis), ctypes.byref(distinct)))
             greedy[net] = {"wall_s": round(wall, 4), "first_call_s": round(first, 4), "visited": visited,
-                           "candidates_per_s": round(visited / wall, 1)}
+                           "candidates_per_s": round(visited / wall, 1),
+                           "distinct_children": int(distinct.value),
+                           "dedup_factor": round(visited / max(1, distinct.value), 3),
+                           "schedule": [d.render() for d in s.decisions]}
+        if not args.no_ref_greedy:
+            try:
+                ref = reference_greedy(list(greedy))
+                for net, (wall, visited, sched) in ref.items():
+                    greedy[net]["reference"] = {
+                        "wall_s": round(wall, 3), "visited": visited,
+                        "identical_schedule": sched == greedy[net]["schedule"] and visited == greedy[net]["visited"],
+                        "kind": "tensched.search.greedy_schedule + model_value (Cython), oracle/_ref, "
+                                "one process per network on this host"}
+                    greedy[net]["speedup_vs_reference"] = round(wall / greedy[net]["wall_s"], 1)
+            except Exception as e:  # reported, never silently replaced
+                greedy["reference"] = f"unavailable: {e}"
+        for g_ in greedy.values():
+            if isinstance(g_, dict):
+                g_.pop("schedule", None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N=1 only
@@ -631,6 +837,8 @@ def main():
             "cpu_baseline": cpu,
             "greedy_wall_s": greedy,
             "sweep_states_per_s": sweep,
+            "exact_leg": exact_leg,
+            "sweep_1e8_one_gpu": big,
             "v_training": train_line,
             "clocks": clk,
         }

@@ -10,6 +10,8 @@
  * Reference interfaces replaced (paths relative to /root/reference/pkg/src/tensched):
  *   ts_lstm_forward        <- backend.lstm_forward / _recurrent_cy.lstm_forward
  *                             (backend.py:26, _recurrent_cy.pyx:20-66)
+ *   ts_lstm_backward       <- backend.lstm_forward_cached + lstm_backward
+ *                             (backend.py:15-16, _recurrent_np.py:38-96)
  *   ts_featurize_states    <- featurizer.featurize_state + normalize
  *                             (featurizer.py:68-107, :136-137)
  *   ts_score_states        <- value_model.predict_states (value_model.py:129-155),
@@ -79,6 +81,18 @@ typedef struct ts_decision {
  * (tcgen05, split-fp16 operands, fp32 TMEM accumulators). */
 #define TS_MODE_EXACT 0
 #define TS_MODE_FAST 1
+/* Operand range of the tensor-core leg.  An operand x is split into
+ * hi = fp16(x), lo = fp16(x - hi): 22 significant bits while |x| stays below
+ * fp16's 65,504, absolute error |x| 2^-22.  A state whose normalized features
+ * leave [-TS_FAST_RANGE, TS_FAST_RANGE] (a sigma-floored normalizer: 1e-6
+ * puts a differing value near 1e6; a pipeline far outside the training data)
+ * is rescored on the exact leg, and a pipeline whose unscheduled rows leave
+ * it is scored on the exact leg altogether, so TS_MODE_FAST never returns a
+ * V computed from clipped or infinite operands.  2^12 keeps a 16x margin
+ * below the fp16 overflow and bounds the operand error at 1e-3; v0 reaches
+ * |x| <= ~600 on any state of the benchmark networks (feature 13, sigma
+ * 0.238), so the guard never fires on it. */
+#define TS_FAST_RANGE 4096.0f
 
 typedef struct ts_ctx ts_ctx;
 
@@ -175,6 +189,17 @@ int ts_lstm_forward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t 
                     const double* Wx, const double* Wh, const double* b, const double* w,
                     int64_t H, double b_out, int mode, double* raw_out);
 
+/* backend.lstm_backward(X, Wx, Wh, w, cache, d_raw) -> (dWx, dWh, db, dw,
+ * db_out) (backend.py:16, _recurrent_np.py:62-96): gradients of
+ * sum_b d_raw[b] * raw[b] for the batch X [B][T][F] (F = 16, C-contiguous).
+ * The forward is recomputed on the device (the reference's per-timestep
+ * activation cache, _recurrent_np.py:38-59, is the host's opaque handle and
+ * carries b and b_out).  fp64 throughout.  grad_out: [dWx F x 4H | dWh
+ * H x 4H | db 4H | dw H | db_out], 4H(F+H+1)+H+1 doubles. */
+int ts_lstm_backward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t F,
+                     const double* Wx, const double* Wh, const double* b, const double* w,
+                     int64_t H, double b_out, const double* d_raw, double* grad_out);
+
 /* candidate_actions for the state given by `prefix` (n_prefix decisions). */
 int ts_candidates(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix,
                   ts_decision* out, int64_t capacity, int64_t* n_out);
@@ -193,6 +218,12 @@ int ts_check_action(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int
  * waits; the call returns with the context's stream idle. */
 int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
               ts_decision* out_decisions, int64_t* visited, double* out_best_v);
+
+/* Dedup statistics of the last ts_greedy call on this context: candidates
+ * visited and distinct children feature rows among them (children with
+ * bit-identical rows share one exact LSTM; visited / distinct is the dedup
+ * factor). */
+int ts_greedy_stats(ts_ctx* ctx, int64_t* visited, int64_t* distinct);
 
 /* One layer step for an arbitrary parent state (the children
  * half of greedy_schedule, search.py:97-110): the parent's n_parent decisions

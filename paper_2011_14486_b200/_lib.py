@@ -100,10 +100,12 @@ def load_library():
             "ts_encode_codes_device": ([vp, i32, vp, vp, i64, vp], i32),
             "ts_encode_codes": ([vp, i32, vp, vp, i64, vp], i32),
             "ts_lstm_forward": ([vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, f64, i32, vp], i32),
+            "ts_lstm_backward": ([vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, f64, vp, vp], i32),
             "ts_candidates": ([vp, i32, vp, i64, vp, i64, ctypes.POINTER(i64)], i32),
             "ts_check_action": ([vp, i32, vp, i64, vp], i32),
             "ts_greedy": ([vp, i32, f64, ctypes.POINTER(ctypes.c_uint64), vp,
                            ctypes.POINTER(i64), ctypes.POINTER(f64)], i32),
+            "ts_greedy_stats": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
             "ts_generate_states_device": ([vp, i32, ctypes.c_uint64, i64, vp, vp,
                                            ctypes.POINTER(i64)], i32),
             "ts_sync": ([vp], i32),

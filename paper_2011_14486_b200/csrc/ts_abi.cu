@@ -100,6 +100,7 @@ struct PipelineSlot {
   DevBuf code_table; // [T][TS_CODE_SPACE + 1] decoded action codes (built on first coded call)
   uint64_t rows_version = 0;  // params version the init rows / prefix belong to
   uint64_t fast_version = 0;
+  bool fast_safe = true;      // unscheduled rows inside the tensor-core operand range
 };
 
 }  // namespace
@@ -150,6 +151,12 @@ struct ts_ctx {
   // the SMs the other chunk's kernel tails leave idle
   cudaStream_t stream2 = nullptr;
   DevBuf reps2, rows2, tile_ctr2, scan_tmp2;
+  DevBuf resc, resc2;  // k_rescore_exact scratch rows, per lane
+  DevBuf bk_X, bk_meta, bk_P;  // ts_lstm_backward: the batch, its layout, params + gradient
+  DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
+  unsigned long long greedy_distinct = 0;
+  int64_t greedy_visited = 0;
+  bool tr_group_attr_set = false;
 };
 
 namespace {
@@ -170,6 +177,7 @@ struct LaneSwap {
     swap_buf(c->rows, c->rows2);
     swap_buf(c->tile_ctr, c->tile_ctr2);
     swap_buf(c->scan_tmp, c->scan_tmp2);
+    swap_buf(c->resc, c->resc2);
   }
 };
 }  // namespace
@@ -426,6 +434,8 @@ int ts_ctx_create(int device, ts_ctx** out) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_featurize_rows<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                max_slot_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_rescore_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, max_slot_smem);
 
     if (e != cudaSuccess) {
       delete ctx;
@@ -640,6 +650,19 @@ static size_t fast_pre_bytes(int T) { return sizeof(float) * (T + 1) * tc::PRE_S
 static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   if (P->fast_version == ctx->params_version) return TS_OK;
   const int T = P->h->n_stages;
+  {  // the unscheduled rows (and every row's intrinsic half) as operands
+    std::vector<double> rows((size_t)T * F);
+    TS_CUDA(cudaMemcpyAsync(rows.data(), P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+    P->fast_safe = true;
+    for (double v : rows)
+      if (!(std::fabs((double)(float)v) <= (double)TS_FAST_RANGE)) P->fast_safe = false;
+    if (!P->fast_safe) {
+      P->fast_version = ctx->params_version;
+      return TS_OK;
+    }
+  }
   TS_CUDA(P->pre_fast.reserve(fast_pre_bytes(T) + sizeof(float) * T * F));
   uint4* initx = reinterpret_cast<uint4*>(P->pre_fast.as<uint8_t>() + fast_pre_bytes(T));
   tc::k_init_split<<<(unsigned)((T + 63) / 64), 64, 0, ctx->stream>>>(P->init_norm.as<double>(), T, initx);
@@ -670,9 +693,22 @@ static int ensure_fast_prefix(ts_ctx* ctx, PipelineSlot* P) {
   return TS_OK;
 }
 
-// FAST scratch of a batch: rowoff[T + 2] (int64), perm[n], hist/cursor[T + 2]
+// FAST scratch of a batch: rowoff[T + 2] (int64), perm[n], hist/cursor[T + 2],
+// the range-guard flags (n bytes, 16-byte aligned and padded)
 static size_t fast_reps_bytes(int T, int64_t n_states) {
-  return sizeof(int64_t) * (T + 2) + sizeof(int) * (n_states + 2 * (T + 2));
+  return sizeof(int64_t) * (T + 2) + sizeof(int) * (n_states + 2 * (T + 2)) + 16 + ((n_states + 15) & ~15ll);
+}
+
+// TS_MODE_FAST on a pipeline whose unscheduled rows leave the tensor-core
+// operand range runs on the exact leg (TS_FAST_RANGE).
+static int resolve_mode(ts_ctx* ctx, PipelineSlot* P, int& mode) {
+  if (mode != TS_MODE_FAST || ctx->hidden != 32) return TS_OK;
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  rc = ensure_fast_prefix(ctx, P);
+  if (rc) return rc;
+  if (!P->fast_safe) mode = TS_MODE_EXACT;
+  return TS_OK;
 }
 
 // d_codes (optional): 16-bit action codes instead of records, same offsets
@@ -726,10 +762,12 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
     int* perm = reinterpret_cast<int*>(rowoff + (T + 2));
     int* hist = perm + n_states;
     int* cursor = hist + (T + 2);
+    uint8_t* range_flag = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(cursor + (T + 2)) + 15) & ~(uintptr_t)15);
     const unsigned g = (unsigned)((n_states + 255) / 256);
     {
       KTimer kt(ctx, TS_K_OTHER);
       TS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (T + 2), ctx->stream));
+      TS_CUDA(cudaMemsetAsync(range_flag, 0, (n_states + 15) & ~15ll, ctx->stream));
       tc::k_depth_hist<<<std::min<unsigned>(g, 4u * ctx->sm_count), 256, sizeof(int) * (T + 1), ctx->stream>>>(
           d_offsets, n_states, T, hist);
       TS_LAUNCHED();
@@ -747,7 +785,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
                                 slot_smem(P, TS_FEAT_BLOCK), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<float>(), ctx->status.as<int>(),
-          perm, rowoff, d_codes);
+          perm, rowoff, d_codes, range_flag);
       TS_LAUNCHED();
     }
     tc::TcArgs ta;
@@ -780,6 +818,16 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
         tc::k_lstm_tc<2><<<grid, 2 * tc::TM, tc::smem_bytes(2), ctx->stream>>>(ta);
       else
         tc::k_lstm_tc<1><<<grid, tc::TM, tc::smem_bytes(1), ctx->stream>>>(ta);
+      TS_LAUNCHED();
+    }
+    {  // range guard: flagged states rescored on the exact leg
+      KTimer kt(ctx, TS_K_OTHER);
+      const int rblocks = ctx->sm_count;
+      TS_CUDA(ctx->resc.reserve(sizeof(double) * F * T * (size_t)rblocks * 4, ctx->stream));
+      k_rescore_exact<<<rblocks, 128, slot_smem(P, 128), ctx->stream>>>(
+          P->d.as<PipelineDesc>(), d_records, d_offsets, d_codes, perm, n_states, P->init_norm.as<double>(),
+          ctx->mean.as<double>(), ctx->stdv.as<double>(), lstm_weights(ctx), P->pre_exact.as<double>(),
+          ctx->target_scale, range_flag, ctx->resc.as<double>(), d_out, ctx->status.as<int>());
       TS_LAUNCHED();
     }
     return TS_OK;
@@ -832,6 +880,10 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, co
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   if (n_states == 0) return TS_OK;
   TS_CUDA(cudaSetDevice(ctx->device));
+  {
+    const int rc0 = resolve_mode(ctx, P, mode);
+    if (rc0) return rc0;
+  }
   const int64_t n_rec = offsets[n_states];
   TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n_rec > 0 ? n_rec : 1)));
   TS_CUDA(ctx->offsets.reserve(sizeof(int64_t) * (n_states + 1)));
@@ -913,6 +965,10 @@ int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed,
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   if (n_states == 0) return TS_OK;
   TS_CUDA(cudaSetDevice(ctx->device));
+  {
+    const int rc0 = resolve_mode(ctx, P, mode);
+    if (rc0) return rc0;
+  }
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
   if (mode == TS_MODE_FAST) {
@@ -993,6 +1049,10 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   if (n_states == 0) return TS_OK;
   TS_CUDA(cudaSetDevice(ctx->device));
+  {
+    const int rc0 = resolve_mode(ctx, P, mode);
+    if (rc0) return rc0;
+  }
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
   if (mode == TS_MODE_FAST) {
@@ -1185,6 +1245,10 @@ int ts_score_states_device(ts_ctx* ctx, int pipeline_id, const ts_decision* d_re
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   if (n_states == 0) return TS_OK;
   TS_CUDA(cudaSetDevice(ctx->device));
+  {
+    const int rc0 = resolve_mode(ctx, P, mode);
+    if (rc0) return rc0;
+  }
   int rc = score_device(ctx, P, d_records, d_offsets, n_states, n_records, mode, d_out_v);
   if (rc) return rc;
   return check_device_status(ctx);
@@ -1198,6 +1262,10 @@ int ts_score_states_coded_device(ts_ctx* ctx, int pipeline_id, const uint16_t* d
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   if (n_states == 0) return TS_OK;
   TS_CUDA(cudaSetDevice(ctx->device));
+  {
+    const int rc0 = resolve_mode(ctx, P, mode);
+    if (rc0) return rc0;
+  }
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
   if (!P->code_table.p) {  // every code of every stage, decoded once per pipeline
@@ -1329,6 +1397,8 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   TS_CUDA(cudaSetDevice(ctx->device));
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
+  TS_CUDA(ctx->gstat.reserve(sizeof(unsigned long long)));
+  TS_CUDA(cudaMemsetAsync(ctx->gstat.p, 0, sizeof(unsigned long long), ctx->stream));
   const PipelineDesc& D = *P->h;
   const int T = D.n_stages;
   std::vector<Nest> nests(T);
@@ -1395,7 +1465,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       k_children_rows_dedup<<<1, 1024, 0, ctx->stream>>>(
           P->d.as<PipelineDesc>(), s, hs, n, cn ? hn : nullptr, P->init_raw.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->reps.as<int>(),
-          ctx->status.as<int>(), ticket);
+          ctx->status.as<int>(), ticket, ctx->gstat.as<unsigned long long>());
       TS_LAUNCHED();
       GreedyTail tail;
       tail.ticket = ticket;
@@ -1472,7 +1542,8 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
         P->init_raw.as<double>(), ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(),
         ctx->status.as<int>());
     TS_LAUNCHED();
-    k_dedup<<<1, 512, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>());
+    k_dedup<<<1, 512, 0, ctx->stream>>>(ctx->rows.as<double>(), n, ctx->reps.as<int>(),
+                                        ctx->gstat.as<unsigned long long>());
     TS_LAUNCHED();
     if (ctx->hidden == 32) {
       // a few warps per block: the children are few and latency-bound
@@ -1529,7 +1600,17 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   if (rng_state && epsilon > 0.0) *rng_state = rng;
   *visited = vis;
   if (out_best_v) *out_best_v = best_v;
+  TS_CUDA(cudaMemcpyAsync(&ctx->greedy_distinct, ctx->gstat.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->greedy_visited = vis;
+  return TS_OK;
+}
+
+int ts_greedy_stats(ts_ctx* ctx, int64_t* visited, int64_t* distinct) {
+  if (!ctx || !visited || !distinct) return TS_ERR_ARG;
+  *visited = ctx->greedy_visited;
+  *distinct = (int64_t)ctx->greedy_distinct;
   return TS_OK;
 }
 
@@ -1872,12 +1953,85 @@ static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs&
   a.target_scale = 0.0;
   a.n_total = 1.0;
   a.partial = nullptr;
+  a.draw_in = nullptr;
   return TS_OK;
 }
 
 int ts_train_set_mode(ts_ctx* ctx, int mode) {
   if (!ctx || (mode != TS_TRAIN_EXACT && mode != TS_TRAIN_TC)) return TS_ERR_ARG;
   ctx->tr_mode = mode;
+  return TS_OK;
+}
+
+// Gradient of the loss over this rank's part of a minibatch whose global size
+// is n_total (d_raw divides by it); written to d_grad (device pointer, or the
+// context's buffer when null).  Data-parallel callers all-reduce d_grad.
+// Forward + BPTT + weight gradients of a filled TrainArgs (batch a.B, longest
+// sequence a.Tmax) into grad, in the context's gradient mode.
+static int launch_grads(ts_ctx* ctx, tr::TrainArgs& a, int mode, double* grad, double* raw_out) {
+  const int64_t B = a.B;
+  const int H = a.H, Tmax = a.Tmax;
+  const tr::Layout L(H);
+  const bool grouped = H == tr::GH && !getenv("TS_TRAIN_WARP");
+  const int64_t K = (int64_t)Tmax * B;
+  if (mode == TS_TRAIN_TC) {
+    // fp64 recurrences, weight gradients on the tensor cores fused into BPTT
+    if (H != tr::GH) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
+    TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * Tmax * tr::CACHE_FIELDS * H, ctx->stream));
+    a.cache = ctx->tr_cache.as<double>();
+    const int nblk = (int)((B + tr::GS - 1) / tr::GS);
+    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * nblk * L.n, ctx->stream));
+    a.partial = ctx->tr_partial.as<double>();
+    if (!ctx->tr_tc_attr_set) {
+      TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(tr::GroupSmem)));
+      ctx->tr_tc_attr_set = true;
+    }
+    tr::k_train_fb_group<true><<<nblk, tr::GTHREADS, sizeof(tr::GroupSmem), ctx->stream>>>(a);
+    TS_LAUNCHED();
+    tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), nblk, L.n, grad);
+    TS_LAUNCHED();
+  } else {
+    TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * Tmax * tr::CACHE_FIELDS * H, ctx->stream));
+    TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * K * (grouped ? tr::PROW : L.G), ctx->stream));
+    a.cache = ctx->tr_cache.as<double>();
+    a.dz = ctx->tr_dz.as<double>();
+    int ksplit;
+    if (grouped) {
+      TS_CUDA(ctx->tr_pvalid.reserve(K, ctx->stream));
+      TS_CUDA(cudaMemsetAsync(ctx->tr_pvalid.p, 0, K, ctx->stream));
+      a.pvalid = ctx->tr_pvalid.as<uint8_t>();
+      // grouped kernels (bit-identical forward/BPTT; weight gradients in the
+      // same pair order within each of ksplit ranges)
+      if (!ctx->tr_group_attr_set) {
+        TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(tr::GroupSmem)));
+        ctx->tr_group_attr_set = true;
+      }
+      tr::k_train_fb_group<false><<<(unsigned)((B + tr::GS - 1) / tr::GS), tr::GTHREADS, sizeof(tr::GroupSmem),
+                                    ctx->stream>>>(a);
+      TS_LAUNCHED();
+      ksplit = (int)std::min<int64_t>(2 * ctx->sm_count, std::max<int64_t>(1, K / 64));
+      TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n, ctx->stream));
+      tr::k_train_wgrad_group<<<ksplit, tr::GTHREADS, sizeof(tr::WgradSmem), ctx->stream>>>(
+          a, ksplit, ctx->tr_partial.as<double>());
+      TS_LAUNCHED();
+    } else {
+      tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
+      TS_LAUNCHED();
+      ksplit = (int)std::min<int64_t>(64, std::max<int64_t>(1, K / 512));
+      TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n, ctx->stream));
+      tr::k_train_wgrad<<<dim3((L.n + 255) / 256, ksplit), 256, 0, ctx->stream>>>(a, ksplit,
+                                                                                 ctx->tr_partial.as<double>());
+      TS_LAUNCHED();
+    }
+    tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
+    TS_LAUNCHED();
+  }
+  if (raw_out) {
+    TS_CUDA(cudaMemcpyAsync(raw_out, a.raw, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   return TS_OK;
 }
 
@@ -1899,71 +2053,87 @@ int ts_train_grads(ts_ctx* ctx, const int32_t* idx, int64_t B, int64_t n_total, 
   tr::TrainArgs a;
   int rc = train_args(ctx, idx, B, a);
   if (rc) return rc;
-  const bool grouped = ctx->tr_H == tr::GH && !getenv("TS_TRAIN_WARP");
-  const int64_t K = (int64_t)ctx->tr_Tmax * B;
-  if (ctx->tr_mode == TS_TRAIN_TC) {
-    // fp64 recurrences, weight gradients on the tensor cores fused into BPTT
-    if (ctx->tr_H != tr::GH) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
-    TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
-    a.cache = ctx->tr_cache.as<double>();
-    a.target_scale = target_scale;
-    a.n_total = (double)n_total;
-    const int nblk = (int)((B + tr::GS - 1) / tr::GS);
-    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * nblk * L.n));
-    a.partial = ctx->tr_partial.as<double>();
-    if (!ctx->tr_tc_attr_set) {
-      TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(tr::GroupSmem)));
-      ctx->tr_tc_attr_set = true;
-    }
-    tr::k_train_fb_group<true><<<nblk, tr::GTHREADS, sizeof(tr::GroupSmem), ctx->stream>>>(a);
-    TS_LAUNCHED();
-    tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), nblk, L.n, grad);
-    TS_LAUNCHED();
-    if (raw_out) {
-      TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
-      TS_CUDA(cudaStreamSynchronize(ctx->stream));
-    }
-    return TS_OK;
-  }
-  TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * ctx->tr_Tmax * tr::CACHE_FIELDS * ctx->tr_H));
-  TS_CUDA(ctx->tr_dz.reserve(sizeof(double) * K * (grouped ? tr::PROW : L.G)));
-  a.cache = ctx->tr_cache.as<double>();
-  a.dz = ctx->tr_dz.as<double>();
   a.target_scale = target_scale;
   a.n_total = (double)n_total;
-  int ksplit;
-  if (grouped) {
-    TS_CUDA(ctx->tr_pvalid.reserve(K));
-    TS_CUDA(cudaMemsetAsync(ctx->tr_pvalid.p, 0, K, ctx->stream));
-    a.pvalid = ctx->tr_pvalid.as<uint8_t>();
-    // grouped kernels (bit-identical forward/BPTT; weight gradients in the
-    // same pair order within each of ksplit ranges)
-    TS_CUDA(cudaFuncSetAttribute(tr::k_train_fb_group<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(tr::GroupSmem)));
-    tr::k_train_fb_group<false><<<(unsigned)((B + tr::GS - 1) / tr::GS), tr::GTHREADS, sizeof(tr::GroupSmem),
-                           ctx->stream>>>(a);
-    TS_LAUNCHED();
-    ksplit = (int)std::min<int64_t>(2 * ctx->sm_count, std::max<int64_t>(1, K / 64));
-    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
-    tr::k_train_wgrad_group<<<ksplit, tr::GTHREADS, sizeof(tr::WgradSmem), ctx->stream>>>(
-        a, ksplit, ctx->tr_partial.as<double>());
-    TS_LAUNCHED();
-  } else {
-    tr::k_train_fb<<<(unsigned)((B * 32 + 127) / 128), 128, 0, ctx->stream>>>(a);
-    TS_LAUNCHED();
-    ksplit = (int)std::min<int64_t>(64, std::max<int64_t>(1, K / 512));
-    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * ksplit * L.n));
-    tr::k_train_wgrad<<<dim3((L.n + 255) / 256, ksplit), 256, 0, ctx->stream>>>(a, ksplit,
-                                                                               ctx->tr_partial.as<double>());
-    TS_LAUNCHED();
+  return launch_grads(ctx, a, ctx->tr_mode, grad, raw_out);
+}
+
+// backend.lstm_backward (_recurrent_np.py:62-96): gradients of
+// sum_b d_raw[b] * raw[b] for a dense batch X [B][T][F] under the given
+// weights, fp64 throughout (the forward is recomputed on the device; the
+// reference's activation cache never crosses the boundary).  Independent of
+// the context's training dataset and parameters.
+int ts_lstm_backward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t Fin, const double* Wx,
+                     const double* Wh, const double* b, const double* w, int64_t H, double b_out,
+                     const double* d_raw, double* grad_out) {
+  if (!ctx || !X || !Wx || !Wh || !b || !w || !d_raw || !grad_out || B < 0 || T < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (Fin != F) return fail(ctx, TS_ERR_ARG, "feature width must be 16");
+  if (H < 1 || H > 32) return fail(ctx, TS_ERR_ARG, "hidden size must be in 1..32");
+  if (B > (int64_t)1 << 30 || T > 4096) return fail(ctx, TS_ERR_ARG, "batch or sequence too long");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  const tr::Layout L((int)H);
+  std::vector<double> flat(L.n);
+  memcpy(flat.data() + L.oWx, Wx, sizeof(double) * F * L.G);
+  memcpy(flat.data() + L.oWh, Wh, sizeof(double) * H * L.G);
+  memcpy(flat.data() + L.ob, b, sizeof(double) * L.G);
+  memcpy(flat.data() + L.ow, w, sizeof(double) * H);
+  flat[L.obout] = b_out;
+  if (B == 0 || T == 0) {  // dWx = dWh = db = dw = 0, db_out = T * sum(d_raw)
+    double s = 0.0;
+    for (int64_t i = 0; i < B; ++i) s += d_raw[i];
+    memset(grad_out, 0, sizeof(double) * L.n);
+    grad_out[L.obout] = (double)T * s;
+    return TS_OK;
   }
-  tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), ksplit, L.n, grad);
-  TS_LAUNCHED();
-  if (raw_out) {
-    TS_CUDA(cudaMemcpyAsync(raw_out, ctx->tr_raw.p, sizeof(double) * B, cudaMemcpyDeviceToHost, ctx->stream));
-    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  // the batch as a training dataset: sequence i = init rows i*T .. i*T+T-1
+  // (no scheduled rows), batch = 0..B-1, d_raw given
+  std::vector<int32_t> meta(3 * B + B);
+  std::vector<int64_t> rb(B, 0);
+  for (int64_t i = 0; i < B; ++i) {
+    meta[i] = (int32_t)(i * T);      // init_base
+    meta[B + i] = (int32_t)T;        // Tlen
+    meta[2 * B + i] = 0;             // depth
+    meta[3 * B + i] = (int32_t)i;    // batch
   }
+  if (B * T > INT32_MAX) return fail(ctx, TS_ERR_ARG, "batch x sequence too large");
+  TS_CUDA(ctx->bk_X.reserve(sizeof(double) * B * T * F, ctx->stream));
+  TS_CUDA(ctx->bk_meta.reserve(sizeof(int32_t) * 4 * B + sizeof(int64_t) * B, ctx->stream));
+  TS_CUDA(ctx->bk_P.reserve(sizeof(double) * (L.n + L.n + 2 * B), ctx->stream));
+  TS_CUDA(ctx->tr_raw.reserve(sizeof(double) * B, ctx->stream));
+  TS_CUDA(ctx->tr_draw.reserve(sizeof(double) * B, ctx->stream));
+  int32_t* dmeta = ctx->bk_meta.as<int32_t>();
+  int64_t* drb = reinterpret_cast<int64_t*>(dmeta + 4 * B);
+  double* dP = ctx->bk_P.as<double>();
+  double* dgrad = dP + L.n;
+  double* ddraw = dgrad + L.n;
+  TS_CUDA(cudaMemcpyAsync(ctx->bk_X.p, X, sizeof(double) * B * T * F, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dmeta, meta.data(), sizeof(int32_t) * 4 * B, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(drb, rb.data(), sizeof(int64_t) * B, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dP, flat.data(), sizeof(double) * L.n, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ddraw, d_raw, sizeof(double) * B, cudaMemcpyHostToDevice, ctx->stream));
+  tr::TrainArgs a;
+  memset(&a, 0, sizeof a);
+  a.D.rows = ctx->bk_X.as<double>();
+  a.D.init = ctx->bk_X.as<double>();
+  a.D.row_base = drb;
+  a.D.init_base = dmeta;
+  a.D.Tlen = dmeta + B;
+  a.D.depth = dmeta + 2 * B;
+  a.D.logt = ddraw;  // unused (draw_in)
+  a.batch = dmeta + 3 * B;
+  a.P = dP;
+  a.draw = ctx->tr_draw.as<double>();
+  a.raw = ctx->tr_raw.as<double>();
+  a.B = (int)B;
+  a.Tmax = (int)T;
+  a.H = (int)H;
+  a.n_total = 1.0;
+  a.draw_in = ddraw;
+  int rc = launch_grads(ctx, a, TS_TRAIN_EXACT, dgrad, nullptr);
+  if (rc) return rc;
+  TS_CUDA(cudaMemcpyAsync(grad_out, dgrad, sizeof(double) * L.n, cudaMemcpyDeviceToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   return TS_OK;
 }
 

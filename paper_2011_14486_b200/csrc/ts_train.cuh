@@ -13,7 +13,8 @@
 // so a bootstrap-style dataset of T+1 prefixes per schedule stores T rows.
 //
 //   k_train_fb     warp per sequence, lane per hidden unit: forward with the
-//                  activation cache, d_raw = 2(raw + ts - log t)/n_total,
+//                  activation cache, d_raw = 2(raw + ts - log t)/n_total (or
+//                  the caller's d_raw: backend.lstm_backward),
 //                  BPTT; writes dz[b][t][4H] and keeps h_prev/h in the cache
 //   k_train_wgrad  split-K weight gradients: block (p-tile, k-split) sums its
 //                  (t, b) range in a fixed order into partials
@@ -75,6 +76,7 @@ struct TrainArgs {
   double target_scale;
   double n_total;       // global minibatch size n (value_model.py:193)
   double* partial;      // tensor-core weight gradients: [gridDim.x][n_params] per-CTA sums
+  const double* draw_in;  // optional [B]: d_raw given by the caller (lstm_backward), else the loss's
 };
 
 __global__ void k_train_fb(TrainArgs a) {
@@ -137,7 +139,8 @@ __global__ void k_train_fb(TrainArgs a) {
     raw = fadd(raw, acc);
   }
   // d_raw = 2 (raw + ts - log t) / n  (value_model.py:201)
-  const double d_raw = fdiv(fmul(2.0, fsub(fadd(raw, a.target_scale), a.D.logt[idx])), a.n_total);
+  const double d_raw = a.draw_in ? a.draw_in[wb]
+                                 : fdiv(fmul(2.0, fsub(fadd(raw, a.target_scale), a.D.logt[idx])), a.n_total);
   if (lane == 0) {
     a.raw[wb] = raw;
     a.draw[wb] = d_raw;
@@ -484,7 +487,8 @@ __global__ void __launch_bounds__(GTHREADS, 2) k_train_fb_group(TrainArgs a) {
     const int b = g0 + warp + 8 * q;
     d_raw[q] = 0.0;
     if (b >= a.B) continue;
-    d_raw[q] = fdiv(fmul(2.0, fsub(fadd(raw[q], a.target_scale), a.D.logt[a.batch[b]])), a.n_total);
+    d_raw[q] = a.draw_in ? a.draw_in[b]
+                         : fdiv(fmul(2.0, fsub(fadd(raw[q], a.target_scale), a.D.logt[a.batch[b]])), a.n_total);
     if (lane == 0) {
       a.raw[b] = raw[q];
       a.draw[b] = d_raw[q];

@@ -245,3 +245,76 @@ def test_tensor_core_training_run(golden, v0_path):
           f"(reference {g['metrics']['holdout_r2']:.6f})")
     assert rel.max() <= 1e-4, rel.max()
     assert abs(metrics["holdout_r2"] - g["metrics"]["holdout_r2"]) < 5e-5
+
+
+# ------------------------------------------------ seam 1: backend.lstm_backward
+def _ref_module(name):
+    import importlib
+    import pathlib
+    import sys
+    ref = pathlib.Path(__file__).resolve().parent.parent / "oracle" / "_ref"
+    if not (ref / "tensched").exists():
+        pytest.skip("oracle/_ref (the built reference) is not present")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    return importlib.import_module(name)
+
+
+@pytest.mark.gpu
+def test_backend_backward_matches_reference_numpy(v0_path):
+    """backend.lstm_forward_cached + lstm_backward on the device against the
+    reference's own numpy BPTT (_recurrent_np.py:38-96) on the same batch:
+    every gradient within 1e-10 of its block norm, raw within 1e-12."""
+    rnp = _ref_module("tensched._recurrent_np")
+    from paper_2011_14486_b200 import backend
+    from paper_2011_14486_b200.value_model import load
+    p = load(v0_path)
+    rng = np.random.default_rng(5)
+    for B, T in ((1, 1), (7, 3), (16, 34), (100, 12), (33, 121)):
+        X = rng.normal(size=(B, T, 16)) * rng.choice([0.0, 1.0, 3.0], size=(B, T, 16))
+        d_raw = rng.normal(size=B) / B
+        raw, cache = backend.lstm_forward_cached(X, p.Wx, p.Wh, p.b, p.w, p.b_out)
+        want_raw, want_cache = rnp.lstm_forward_cached(X, p.Wx, p.Wh, p.b, p.w, p.b_out)
+        np.testing.assert_allclose(raw, want_raw, rtol=1e-12, atol=1e-13)
+        got = backend.lstm_backward(X, p.Wx, p.Wh, p.w, cache, d_raw)
+        want = rnp.lstm_backward(X, p.Wx, p.Wh, p.w, want_cache, d_raw)
+        for name, g, w in zip(("dWx", "dWh", "db", "dw", "db_out"), got, want):
+            g, w = np.atleast_1d(g), np.atleast_1d(w)
+            err = np.linalg.norm(g - w) / max(np.linalg.norm(w), 1e-300)
+            assert err < 1e-10, (B, T, name, err)
+
+
+@pytest.mark.gpu
+def test_unmodified_reference_train_on_cuda_backend(golden, v0_path, monkeypatch):
+    """INTEGRATION.md level 2: the unmodified reference's value_model.train
+    (value_model.py:223-293) with its kernel seam switched to this backend
+    (lstm_forward, lstm_forward_cached, lstm_backward on the B200) on the v0
+    dataset and config reproduces the reference-trained v0: V within 1e-4 on
+    the dataset, holdout R^2 within 5e-5."""
+    rbk = _ref_module("tensched.backend")
+    rvm = _ref_module("tensched.value_model")
+    rpi = _ref_module("tensched.pipeline_ir")
+    rss = _ref_module("tensched.schedule_space")
+    from paper_2011_14486_b200 import backend
+    from paper_2011_14486_b200.value_model import load, predict_states
+    monkeypatch.setattr(rbk, "lstm_forward", backend.lstm_forward)
+    monkeypatch.setattr(rbk, "lstm_forward_cached", backend.lstm_forward_cached)
+    monkeypatch.setattr(rbk, "lstm_backward", backend.lstm_backward)
+    monkeypatch.setattr(rbk, "BACKEND", "cuda")
+    g = json.loads((golden / "train_v0.json").read_text())
+    pipes = {n: rpi.parse_pipeline(t) for n, t in g["pipelines"].items()}
+    data = [(rss.state_from_key(pipes[k.split("/", 1)[0]], k), float.fromhex(t))
+            for k, t in zip(g["keys"], g["targets"])]
+    c = g["config"]
+    cfg = rvm.TrainConfig(c["learning_rate"], c["epochs"], c["batch_size"], c["seed"], c["clip_norm"],
+                          c["holdout_fraction"], c["patience"])
+    trained, metrics = rvm.train(rvm.init_params(c["seed"], c["hidden"]), data, cfg)
+    ref = load(v0_path)
+    assert trained.target_scale == ref.target_scale
+    _, ours = _dataset(golden)
+    states = [s for s, _ in ours]
+    rel = np.abs(predict_states(trained, states) / predict_states(ref, states) - 1)
+    print(f"reference train() on the cuda backend: max |V/V_v0 - 1| = {rel.max():.2e}, holdout R^2 "
+          f"{metrics['holdout_r2']:.6f} (reference {g['metrics']['holdout_r2']:.6f})")
+    assert rel.max() <= 1e-4, rel.max()
+    assert abs(metrics["holdout_r2"] - g["metrics"]["holdout_r2"]) < 5e-5
