@@ -531,10 +531,16 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank (LOCAL_RANK); TS_DEVICE / TS_DIST_BACKEND=gloo let the
+    # multi-process test run two ranks on one GPU (correctness only)
+    local = int(os.environ.get("TS_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    backend = os.environ.get("TS_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2011_14486_b200 import _lib
     from paper_2011_14486_b200.pipeline_ir import parse_pipeline
