@@ -234,29 +234,35 @@ def _ref_cost_worker(args):
     return n / (time.perf_counter() - t0)
 
 
-def _ref_greedy_worker(net):
-    """The reference's own greedy_schedule with its model_value V-callable
+def _ref_search_worker(task):
+    """The reference's own search with its model_value V-callable
     (cli.py:cmd_schedule's timed region, cli.py:226-232) on one benchmark
-    network, v0.ckpt: wall time, visited count and the schedule."""
+    network, v0.ckpt: greedy_schedule, or beam_search(initial_state, V, 8)
+    for ("beam", net).  Wall time, visited count (greedy) and the schedule."""
+    kind, net = task
     _ref_import()
     from tensched.pipeline_ir import parse_pipeline
-    from tensched.search import greedy_schedule, model_value
+    from tensched.schedule_space import initial_state
+    from tensched.search import beam_search, greedy_schedule, model_value
     from tensched.value_model import load
     params = load(str(GOLD / "v0.ckpt"))
     p = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
     V = model_value(params)
     t0 = time.perf_counter()
-    s, visited = greedy_schedule(p, V)
+    if kind == "beam":
+        s, visited = beam_search(initial_state(p), V, 8), None
+    else:
+        s, visited = greedy_schedule(p, V)
     wall = time.perf_counter() - t0
-    return net, wall, visited, [d.render() for d in s.decisions]
+    return task, wall, visited, [d.render() for d in s.decisions]
 
 
-def reference_greedy(nets):
-    """One process per network (they run side by side on the host's cores;
-    each wall time is its own process's)."""
+def reference_search(tasks):
+    """One process per (kind, network) task (they run side by side on the
+    host's cores; each wall time is its own process's)."""
     import multiprocessing as mp
-    with mp.get_context("spawn").Pool(len(nets)) as pool:
-        return {r[0]: r[1:] for r in pool.map(_ref_greedy_worker, nets)}
+    with mp.get_context("spawn").Pool(len(tasks)) as pool:
+        return {r[0]: r[1:] for r in pool.map(_ref_search_worker, tasks)}
 
 
 def run_reference_arm(args):
@@ -769,7 +775,7 @@ def main():
     if not args.no_train:
         train_line = train_throughput(ctx, pid, inf, params, rank, world, dev, args)
 
-    greedy = {}
+    greedy, beam = {}, {}
     if rank == 0 and not args.no_greedy:
         from paper_2011_14486_b200.search import greedy_schedule_gpu
         for net in ("crp2d", "resnet18", "resnet50", "mobilenet_v2"):
@@ -787,19 +793,33 @@ def main():
                            "distinct_children": int(distinct.value),
                            "dedup_factor": round(visited / max(1, distinct.value), 3),
                            "schedule": [d.render() for d in s.decisions]}
+        from paper_2011_14486_b200.schedule_space import initial_state
+        from paper_2011_14486_b200.search import beam_search_gpu
+        for net in ("vgg16", "resnet18"):  # beam_search(initial_state, model_value(v0), 8)
+            pn = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
+            t0 = time.perf_counter()
+            beam_search_gpu(initial_state(pn), params, 8)
+            first = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            s = beam_search_gpu(initial_state(pn), params, 8)
+            beam[net] = {"wall_s": round(time.perf_counter() - t0, 4), "first_call_s": round(first, 4),
+                         "width": 8, "schedule": [d.render() for d in s.decisions]}
         if not args.no_ref_greedy:
             try:
-                ref = reference_greedy(list(greedy))
-                for net, (wall, visited, sched) in ref.items():
-                    greedy[net]["reference"] = {
+                tasks = [("greedy", n) for n in greedy] + [("beam", n) for n in beam]
+                ref = reference_search(tasks)
+                for (kind, net), (wall, visited, sched) in ref.items():
+                    mine = greedy[net] if kind == "greedy" else beam[net]
+                    mine["reference"] = {
                         "wall_s": round(wall, 3), "visited": visited,
-                        "identical_schedule": sched == greedy[net]["schedule"] and visited == greedy[net]["visited"],
-                        "kind": "tensched.search.greedy_schedule + model_value (Cython), oracle/_ref, "
-                                "one process per network on this host"}
-                    greedy[net]["speedup_vs_reference"] = round(wall / greedy[net]["wall_s"], 1)
+                        "identical_schedule": sched == mine["schedule"] and (
+                            kind == "beam" or visited == mine["visited"]),
+                        "kind": f"tensched.search.{'greedy_schedule' if kind == 'greedy' else 'beam_search'}"
+                                " + model_value (Cython), oracle/_ref, one process per task on this host"}
+                    mine["speedup_vs_reference"] = round(wall / mine["wall_s"], 1)
             except Exception as e:  # reported, never silently replaced
                 greedy["reference"] = f"unavailable: {e}"
-        for g_ in greedy.values():
+        for g_ in list(greedy.values()) + list(beam.values()):
             if isinstance(g_, dict):
                 g_.pop("schedule", None)
 
@@ -842,6 +862,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "greedy_wall_s": greedy,
+            "beam_wall_s": beam,
             "sweep_states_per_s": sweep,
             "exact_leg": exact_leg,
             "sweep_1e8_one_gpu": big,

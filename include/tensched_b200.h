@@ -240,6 +240,16 @@ int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, i
                       const ts_decision* children, int64_t n_children, double epsilon, uint64_t* rng_state,
                       double* out_v, int64_t* out_best, double* out_best_v);
 
+/* beam_search(prefix, model_value(params), width) (search.py:115-133),
+ * fused per layer: every frontier state's children enumerated natively,
+ * their new rows, per-parent dedup and the exact fp64 LSTM in one device
+ * pass, ranked by (V, index); the `width` best form the next frontier.
+ * out_decisions: the T decisions of the returned complete state (the
+ * prefix's first); visited: children scored; out_v: its V.  Hidden size 32.
+ * Width 1 is the noiseless greedy from the prefix. */
+int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix, int width,
+            ts_decision* out_decisions, int64_t* visited, double* out_v);
+
 /* Device-side random partial states (the synthetic sweep generator): state i
  * walks uniformly over candidate_actions with SearchRng(seed0 + i) after
  * drawing its depth d = randrange(T) + 1 (search.py:136-142 variant).

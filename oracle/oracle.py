@@ -350,6 +350,20 @@ def greedy(P: Pipe, params, epsilon=0.0, rng=None):
     return decisions, visited
 
 
+def beam(P: Pipe, params, prefix, width):
+    """search.py:115-133 with the oracle V: children of every frontier state
+    in frontier order, ranked by (v, index), the `width` best kept; the
+    final V(frontier) argmin by (v, index).  Returns the decisions."""
+    frontier = [list(prefix)]
+    while len(frontier[0]) < len(P.topo):
+        children = [f + [a] for f in frontier for a in candidates(P, f)]
+        vals = list(values(params, P, children))
+        ranked = sorted(range(len(children)), key=lambda i: (float(vals[i]), i))
+        frontier = [children[i] for i in ranked[:width]]
+    vals = list(values(params, P, frontier))
+    return frontier[min(range(len(frontier)), key=lambda i: (float(vals[i]), i))]
+
+
 def random_partial(P: Pipe, seed: int):
     """Synthetic-sweep state: SearchRng(seed), d = randrange(T) + 1, then d
     uniform candidate choices (search.py:136-142 variant)."""

@@ -106,6 +106,7 @@ def load_library():
             "ts_greedy": ([vp, i32, f64, ctypes.POINTER(ctypes.c_uint64), vp,
                            ctypes.POINTER(i64), ctypes.POINTER(f64)], i32),
             "ts_greedy_stats": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+            "ts_beam": ([vp, i32, vp, i64, i32, vp, ctypes.POINTER(i64), ctypes.POINTER(f64)], i32),
             "ts_generate_states_device": ([vp, i32, ctypes.c_uint64, i64, vp, vp,
                                            ctypes.POINTER(i64)], i32),
             "ts_sync": ([vp], i32),

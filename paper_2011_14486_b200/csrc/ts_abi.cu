@@ -154,6 +154,8 @@ struct ts_ctx {
   DevBuf resc, resc2;  // k_rescore_exact scratch rows, per lane
   DevBuf bk_X, bk_meta, bk_P;  // ts_lstm_backward: the batch, its layout, params + gradient
   DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
+  DevBuf beam_rows;             // ts_beam: frontier state rows, double-buffered
+  HostBuf h_sel;                // ts_beam: the next frontier's (parent, child) pairs
   unsigned long long greedy_distinct = 0;
   int64_t greedy_visited = 0;
   bool tr_group_attr_set = false;
@@ -1500,7 +1502,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
                                    (const double*)P->pre_exact.as<double>(), T, s,
                                    (const double*)ctx->rows.as<double>(), (const int*)ctx->reps.as<int>(), n,
                                    (const double*)state_rows, ctx->raw.as<double>(), (const double*)zx_state,
-                                   tail));
+                                   tail, (const int*)nullptr));
       }
       TS_LAUNCHED();
       const double tw0 = trace ? now_us() : 0.0;
@@ -1734,6 +1736,190 @@ int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, i
     if (out_best_v) *out_best_v = ho[0];
     if (rng_state && epsilon > 0.0) *rng_state = rng + (uint64_t)n * 0x9E3779B97F4A7C15ull;
   }
+  return TS_OK;
+}
+
+// beam_search (search.py:115-133) from a prefix, fused per layer: the
+// children of every frontier state are enumerated on the host (native
+// candidate_actions, the frontier's nests kept incrementally) and scored in
+// ONE device pass - each child's new row (one thread each, its parent's
+// consumer nest), dedup of bit-identical rows inside each parent's children,
+// the exact fp64 LSTM from the shared unscheduled prefix through the new row
+// and the parent's rows (one CTA per distinct child, the parent's rows
+// selected per child) - then ranked on the host by (V, index) exactly as
+// sorted(range, key=(v, i)) and the `width` best become the next frontier
+// (their state rows assembled on the device).  Returns frontier[0] of the
+// last layer: the reference's final V(frontier) re-scores the same states
+// and its argmin by (v, i) is that entry.
+int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_prefix, int width,
+            ts_decision* out_decisions, int64_t* visited, double* out_v) {
+  if (!ctx || (n_prefix > 0 && !prefix) || !out_decisions || n_prefix < 0) return TS_ERR_ARG;
+  TS_NEED_DEVICE();
+  if (width < 1) return fail(ctx, TS_ERR_PIPELINE, "beam width must be >= 1");
+  if (width > 1024) return fail(ctx, TS_ERR_ARG, "beam width above 1024");
+  PipelineSlot* P = get_pipe(ctx, pipeline_id);
+  if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
+  if (ctx->hidden != 32) return fail(ctx, TS_ERR_ARG, "the fused beam needs hidden size 32");
+  const PipelineDesc& D = *P->h;
+  const int T = D.n_stages;
+  if (n_prefix > T) return fail(ctx, TS_ERR_ILLEGAL, "prefix longer than the pipeline");
+  TS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_pipe_ready(ctx, P);
+  if (rc) return rc;
+  struct Entry {
+    std::vector<ts_decision> decs;
+    std::vector<Nest> nests;
+  };
+  std::vector<Entry> frontier(1);
+  rc = host_nests(ctx, D, prefix, n_prefix, frontier[0].nests);
+  if (rc) return rc;
+  frontier[0].decs.assign(prefix, prefix + n_prefix);
+  if (visited) *visited = 0;
+  const int d0 = (int)n_prefix;
+  if (d0 == T) {  // complete: the prefix itself (V through the scoring path)
+    memcpy(out_decisions, prefix, sizeof(ts_decision) * T);
+    if (out_v) {
+      const int64_t offs[2] = {0, T};
+      return ts_score_states(ctx, pipeline_id, prefix, offs, 1, TS_MODE_EXACT, out_v);
+    }
+    return TS_OK;
+  }
+  // device state rows of the frontier, double-buffered: [width][T][F]
+  const size_t frow = (size_t)T * F;
+  TS_CUDA(ctx->beam_rows.reserve(sizeof(double) * frow * 2 * width));
+  TS_CUDA(ctx->h_sel.reserve(sizeof(int) * 2 * width));
+  double* cur = ctx->beam_rows.as<double>();
+  double* nxt = cur + frow * width;
+  TS_CUDA(cudaMemcpyAsync(cur, P->init_norm.p, sizeof(double) * frow, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (d0) {  // the prefix's scheduled rows
+    TS_CUDA(ctx->tmp.reserve(sizeof(double) * d0 * F + sizeof(ts_decision) * d0 + 2 * sizeof(int64_t)));
+    double* prow = ctx->tmp.as<double>();
+    ts_decision* d_pre = reinterpret_cast<ts_decision*>(prow + (size_t)d0 * F);
+    int64_t* d_off = reinterpret_cast<int64_t*>(d_pre + d0);
+    const int64_t hoff[2] = {0, d0};
+    TS_CUDA(cudaMemcpyAsync(d_pre, prefix, sizeof(ts_decision) * d0, cudaMemcpyHostToDevice, ctx->stream));
+    TS_CUDA(cudaMemcpyAsync(d_off, hoff, sizeof(hoff), cudaMemcpyHostToDevice, ctx->stream));
+    k_featurize_rows<double><<<1, 128, slot_smem(P, 128), ctx->stream>>>(
+        P->d.as<PipelineDesc>(), d_pre, d_off, 1, P->init_norm.as<double>(), ctx->mean.as<double>(),
+        ctx->stdv.as<double>(), prow, ctx->status.as<int>());
+    TS_LAUNCHED();
+    k_parent_rows<<<(d0 * F + 127) / 128, 128, 0, ctx->stream>>>(prow, d0, T, cur);
+    TS_LAUNCHED();
+  }
+  std::vector<ts_decision> cands;
+  std::vector<int> parent_of, seg;
+  std::vector<std::pair<double, int>> ranked;
+  int64_t vis = 0;
+  for (int i = d0; i < T; ++i) {
+    const int s = T - 1 - i;
+    const StageDesc& sd = D.st[s];
+    const StageDesc* cs = sd.consumer >= 0 ? &D.st[sd.consumer] : nullptr;
+    const int W = (int)frontier.size();
+    cands.clear();
+    parent_of.clear();
+    seg.assign(1, 0);
+    for (int w = 0; w < W; ++w) {
+      const Nest* cn = cs ? &frontier[w].nests[sd.consumer] : nullptr;
+      const int64_t cnt = enumerate_candidates(sd, cs, cn, [&](const ts_decision& d) {
+        cands.push_back(d);
+        parent_of.push_back(w);
+      });
+      if (cnt <= 0) return fail(ctx, cnt < 0 ? (int)-cnt : TS_ERR_PIPELINE, "candidate enumeration");
+      if (cnt > 4096) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
+      seg.push_back((int)cands.size());
+    }
+    const int n = (int)cands.size();
+    vis += n;
+    // pinned staging: records | parent_of | seg | consumer nests (one H2D)
+    const size_t b_rec = sizeof(ts_decision) * n, b_par = sizeof(int) * n, b_seg = sizeof(int) * (W + 1);
+    const size_t o_par = b_rec, o_seg = o_par + b_par, o_nest = (o_seg + b_seg + 15) & ~(size_t)15;
+    const size_t b_all = o_nest + sizeof(Nest) * W;
+    TS_CUDA(ctx->h_stage.reserve(b_all));  // its last H2D finished at the previous sync
+    TS_CUDA(ctx->records.reserve(b_all, ctx->stream));
+    uint8_t* hb = ctx->h_stage.as<uint8_t>();
+    memcpy(hb, cands.data(), b_rec);
+    memcpy(hb + o_par, parent_of.data(), b_par);
+    memcpy(hb + o_seg, seg.data(), b_seg);
+    Nest* hn = reinterpret_cast<Nest*>(hb + o_nest);
+    if (cs)
+      for (int w = 0; w < W; ++w) hn[w] = frontier[w].nests[sd.consumer];
+    uint8_t* db = ctx->records.as<uint8_t>();
+    TS_CUDA(cudaMemcpyAsync(db, hb, b_all, cudaMemcpyHostToDevice, ctx->stream));
+    const ts_decision* d_c = reinterpret_cast<const ts_decision*>(db);
+    const int* d_par = reinterpret_cast<const int*>(db + o_par);
+    const int* d_seg = reinterpret_cast<const int*>(db + o_seg);
+    const Nest* d_nest = cs ? reinterpret_cast<const Nest*>(db + o_nest) : nullptr;
+    TS_CUDA(ctx->rows.reserve(sizeof(double) * F * n, ctx->stream));
+    TS_CUDA(ctx->reps.reserve(sizeof(int) * n, ctx->stream));
+    TS_CUDA(ctx->raw.reserve(sizeof(double) * 2 * n, ctx->stream));
+    double* raw = ctx->raw.as<double>();
+    k_children_rows<<<(n + 127) / 128, 128, 0, ctx->stream>>>(
+        P->d.as<PipelineDesc>(), s, d_c, n, d_nest, P->init_raw.as<double>(), ctx->mean.as<double>(),
+        ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>(), d_par);
+    TS_LAUNCHED();
+    k_dedup_segments<<<W, 512, 0, ctx->stream>>>(ctx->rows.as<double>(), d_seg, ctx->reps.as<int>());
+    TS_LAUNCHED();
+    const size_t xs_bytes = exact_mw_smem(T, s, false);
+    if (xs_bytes > 40 * 1024)
+      TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)xs_bytes));
+    k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
+                                                           ctx->rows.as<double>(), ctx->reps.as<int>(), n, cur,
+                                                           raw, nullptr, GreedyTail{}, d_par);
+    TS_LAUNCHED();
+    double* dv = raw + n;
+    k_children_v<<<(n + 127) / 128, 128, 0, ctx->stream>>>(raw, ctx->reps.as<int>(), n, ctx->target_scale, dv);
+    TS_LAUNCHED();
+    TS_CUDA(ctx->h_out.reserve(sizeof(double) * n + sizeof(int)));
+    double* hv = ctx->h_out.as<double>();
+    TS_CUDA(cudaMemcpyAsync(hv, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    int* hst = reinterpret_cast<int*>(hv + n);
+    TS_CUDA(cudaMemcpyAsync(hst, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (*hst) {
+      const int st = *hst;
+      cudaMemset(ctx->status.p, 0, sizeof(int));
+      return fail(ctx, st, std::string("device: ") + status_name(st));
+    }
+    // sorted(range(len(children)), key=(v, i))[:width]
+    ranked.resize(n);
+    for (int c = 0; c < n; ++c) ranked[c] = {hv[c], c};
+    const int keep = std::min(width, n);
+    std::partial_sort(ranked.begin(), ranked.begin() + keep, ranked.end(),
+                      [](const std::pair<double, int>& a, const std::pair<double, int>& b) {
+                        return a.first < b.first || (a.first == b.first && a.second < b.second);
+                      });
+    std::vector<Entry> next(keep);
+    std::vector<int> sel(2 * keep);
+    for (int k = 0; k < keep; ++k) {
+      const int c = ranked[k].second, w = parent_of[c];
+      sel[2 * k] = w;
+      sel[2 * k + 1] = c;
+      next[k].decs = frontier[w].decs;
+      next[k].decs.push_back(cands[c]);
+      next[k].nests = frontier[w].nests;
+      int64_t pe[TS_MAX_PURE];
+      const int brc = build_nest(sd, cands[c].anchor >= 0 ? cs : nullptr,
+                                 cands[c].anchor >= 0 ? &frontier[w].nests[sd.consumer] : nullptr, cands[c],
+                                 next[k].nests[s], pe);
+      if (brc) return fail(ctx, brc, status_name(brc));
+    }
+    if (i + 1 < T) {  // the next frontier's state rows
+      // (own pinned buffer: its H2D completes before the next layer's sync,
+      // the only point after which the host rewrites it)
+      int* hsel = ctx->h_sel.as<int>();
+      memcpy(hsel, sel.data(), sizeof(int) * 2 * keep);
+      TS_CUDA(cudaMemcpyAsync(ctx->records.p, hsel, sizeof(int) * 2 * keep, cudaMemcpyHostToDevice, ctx->stream));
+      k_beam_advance<<<keep, 256, 0, ctx->stream>>>(cur, nxt, T, s, ctx->records.as<int>(), ctx->rows.as<double>());
+      TS_LAUNCHED();
+      std::swap(cur, nxt);
+    }
+    frontier.swap(next);
+    if (i + 1 == T && out_v) *out_v = ranked[0].first;
+  }
+  memcpy(out_decisions, frontier[0].decs.data(), sizeof(ts_decision) * T);
+  if (visited) *visited = vis;
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   return TS_OK;
 }
 

@@ -74,6 +74,8 @@ def model_value(params, jobs: int = 1, mode: int = MODE_EXACT):
     def fn(states):
         return predict_states(params, states, jobs=jobs, mode=mode)
     if mode == MODE_EXACT:
+        if int(params.hidden) == 32:  # the fused device beam (ts_beam)
+            fn.beam = lambda prefix, width: beam_search_gpu(prefix, params, width)
         fn.score_children = lambda s, actions: (
             score_children(params, s, actions) if len(actions) <= 4096
             else predict_states(params, [child_state(s, a) for a in actions], jobs=jobs, mode=mode))
@@ -171,9 +173,15 @@ def greedy_schedule_gpu(p, params, noise: NoiseConfig | None = None,
 
 
 def beam_search(prefix, V, width: int = 8):
-    """Beam over completions of `prefix` (search.py:115-133)."""
+    """Beam over completions of `prefix` (search.py:115-133).  A model_value
+    V-callable carries the fused device beam (ts_beam: one device pass per
+    layer for all parents' children, no per-child host states); any other V
+    goes through the generic loop below."""
     if width < 1:
         raise PipelineError("beam width must be >= 1")
+    fused = getattr(V, "beam", None)
+    if fused is not None:
+        return fused(prefix, width)
     frontier = [prefix]
     while not frontier[0].is_complete:
         # one device batch per layer for all parents' children (per-parent
@@ -187,6 +195,33 @@ def beam_search(prefix, V, width: int = 8):
     vals = V(frontier)
     best = min(range(len(frontier)), key=lambda i: (float(vals[i]), i))
     return frontier[best]
+
+
+def beam_search_gpu(prefix, params, width: int = 8, device=None, return_value=False):
+    """Fused device beam_search(prefix, model_value(params), width)
+    (ts_beam); the returned state's decisions are the prefix's followed by
+    the completion.  (state[, V of the state])."""
+    if width < 1:
+        raise PipelineError("beam width must be >= 1")
+    p = prefix.pipeline
+    inf = _info(p)
+    ctx = _lib.context(device)
+    pre = np.frombuffer(inf.records_of(prefix), dtype=_lib.DECISION_DTYPE)
+    out = np.zeros(inf.T, dtype=_lib.DECISION_DTYPE)
+    visited = ctypes.c_int64()
+    best_v = ctypes.c_double()
+    with ctx.lock:  # params upload and the beam that scores with them
+        ctx.set_params(params)
+        pid = ctx.pipeline_id(inf.desc)
+        ctx.check(ctx.lib.ts_beam(ctx.h, pid, _lib._p(pre) if len(pre) else None, len(pre), int(width),
+                                  _lib._p(out), ctypes.byref(visited), ctypes.byref(best_v)))
+    d = len(prefix.decisions)
+    s = ScheduleState(p, tuple(prefix.decisions) + tuple(inf.decode(i, rec) for i, rec in enumerate(out)
+                                                         if i >= d))
+    s._cache["ts_records"] = out.tobytes()
+    if return_value:
+        return s, best_v.value
+    return s
 
 
 def random_schedule(p, rng: SearchRng):
