@@ -308,6 +308,11 @@ int ts_train_apply(ts_ctx* ctx, const double* d_grad, double lr, double clip_nor
  * accumulation in TMEM, fused into BPTT; hidden size 32 only). */
 #define TS_TRAIN_EXACT 0
 #define TS_TRAIN_TC 1
+/* TS_TRAIN_TCF: the forward and BPTT recurrences on the tensor cores too
+ * (split-fp16 UMMAs, fp32 accumulation, MUFU gates, a power-of-two scaled
+ * backward; ts_train_tc.cuh) - fp32-accurate gradients, not the fp64
+ * trajectory; hidden size 32 only. */
+#define TS_TRAIN_TCF 2
 int ts_train_set_mode(ts_ctx* ctx, int mode);
 /* raw scores of dataset entries idx[0..n) (for _eval_split). */
 int ts_train_forward(ts_ctx* ctx, const int32_t* idx, int64_t n, double* raw_out);

@@ -28,6 +28,7 @@
 #include "ts_kernels.cuh"
 #include "ts_lstm_tc.cuh"
 #include "ts_train.cuh"
+#include "ts_train_tc.cuh"
 #include "ts_cost.cuh"
 
 using namespace ts;
@@ -154,6 +155,8 @@ struct ts_ctx {
   DevBuf resc, resc2;  // k_rescore_exact scratch rows, per lane
   DevBuf bk_X, bk_meta, bk_P;  // ts_lstm_backward: the batch, its layout, params + gradient
   DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
+  DevBuf trc_img;               // TS_TRAIN_TCF: per-step packed weight images
+  bool trc_attr_set = false;
   DevBuf beam_rows;             // ts_beam: frontier state rows, double-buffered
   HostBuf h_sel;                // ts_beam: the next frontier's (parent, child) pairs
   unsigned long long greedy_distinct = 0;
@@ -2144,7 +2147,7 @@ static int train_args(ts_ctx* ctx, const int32_t* idx, int64_t B, tr::TrainArgs&
 }
 
 int ts_train_set_mode(ts_ctx* ctx, int mode) {
-  if (!ctx || (mode != TS_TRAIN_EXACT && mode != TS_TRAIN_TC)) return TS_ERR_ARG;
+  if (!ctx || (mode != TS_TRAIN_EXACT && mode != TS_TRAIN_TC && mode != TS_TRAIN_TCF)) return TS_ERR_ARG;
   ctx->tr_mode = mode;
   return TS_OK;
 }
@@ -2160,7 +2163,44 @@ static int launch_grads(ts_ctx* ctx, tr::TrainArgs& a, int mode, double* grad, d
   const tr::Layout L(H);
   const bool grouped = H == tr::GH && !getenv("TS_TRAIN_WARP");
   const int64_t K = (int64_t)Tmax * B;
-  if (mode == TS_TRAIN_TC) {
+  if (mode == TS_TRAIN_TCF) {
+    // forward and backward recurrences on the tensor cores (ts_train_tc.cuh)
+    if (H != trc::H) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
+    const int n_tiles = (int)((B + trc::TM - 1) / trc::TM);
+    const size_t img_bytes = tc::TILE_BYTES + 128 + 2 * trc::WT_BYTES;
+    TS_CUDA(ctx->trc_img.reserve(img_bytes, ctx->stream));
+    TS_CUDA(ctx->tr_cache.reserve(sizeof(float) * (size_t)n_tiles * Tmax * trc::NF * 4 * trc::TM * 8, ctx->stream));
+    TS_CUDA(ctx->tr_partial.reserve(sizeof(double) * (size_t)n_tiles * L.n + 16, ctx->stream));
+    if (!ctx->trc_attr_set) {
+      TS_CUDA(cudaFuncSetAttribute(trc::k_trc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, trc::FWD_SMEM));
+      TS_CUDA(cudaFuncSetAttribute(trc::k_trc_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, trc::BWD_SMEM));
+      ctx->trc_attr_set = true;
+    }
+    trc::Args ta;
+    ta.D = a.D;
+    ta.batch = a.batch;
+    ta.B = (int)B;
+    ta.Tmax = Tmax;
+    ta.wimg = ctx->trc_img.as<uint8_t>();
+    ta.P = a.P;
+    ta.cache = ctx->tr_cache.as<float>();
+    ta.raw = a.raw;
+    ta.draw = a.draw;
+    ta.target_scale = a.target_scale;
+    ta.n_total = a.n_total;
+    ta.draw_in = a.draw_in;
+    ta.partial = ctx->tr_partial.as<double>();
+    ta.dmax = reinterpret_cast<unsigned*>(ctx->tr_partial.as<double>() + (size_t)n_tiles * L.n);
+    TS_CUDA(cudaMemsetAsync(ta.dmax, 0, sizeof(unsigned), ctx->stream));
+    trc::k_trc_pack<<<32, 256, 0, ctx->stream>>>(a.P, ctx->trc_img.as<uint8_t>());
+    TS_LAUNCHED();
+    trc::k_trc_fwd<<<n_tiles, trc::FWD_THREADS, trc::FWD_SMEM, ctx->stream>>>(ta);
+    TS_LAUNCHED();
+    trc::k_trc_bwd<<<n_tiles, trc::BWD_THREADS, trc::BWD_SMEM, ctx->stream>>>(ta);
+    TS_LAUNCHED();
+    tr::k_train_reduce<<<(L.n + 63) / 64, 64, 0, ctx->stream>>>(ctx->tr_partial.as<double>(), n_tiles, L.n, grad);
+    TS_LAUNCHED();
+  } else if (mode == TS_TRAIN_TC) {
     // fp64 recurrences, weight gradients on the tensor cores fused into BPTT
     if (H != tr::GH) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
     TS_CUDA(ctx->tr_cache.reserve(sizeof(double) * B * Tmax * tr::CACHE_FIELDS * H, ctx->stream));

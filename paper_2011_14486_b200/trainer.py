@@ -52,7 +52,7 @@ def unflat_into(params, flat: np.ndarray):
     return params
 
 
-TRAIN_MODES = {"exact": 0, "tc": 1}  # TS_TRAIN_EXACT, TS_TRAIN_TC
+TRAIN_MODES = {"exact": 0, "tc": 1, "tcf": 2}  # TS_TRAIN_EXACT, TS_TRAIN_TC, TS_TRAIN_TCF
 
 
 def shard(batch: np.ndarray, rank: int, world: int) -> np.ndarray:

@@ -318,3 +318,74 @@ def test_unmodified_reference_train_on_cuda_backend(golden, v0_path, monkeypatch
           f"{metrics['holdout_r2']:.6f} (reference {g['metrics']['holdout_r2']:.6f})")
     assert rel.max() <= 1e-4, rel.max()
     assert abs(metrics["holdout_r2"] - g["metrics"]["holdout_r2"]) < 5e-5
+
+
+@pytest.mark.gpu
+def test_tensor_core_recurrences_gradients(golden, v0_path):
+    """mode "tcf": forward AND BPTT on the tensor cores (split-fp16 UMMAs,
+    fp32 TMEM accumulation, MUFU gates, power-of-two scaled backward) against
+    the fp64 exact gradients: raw within 1e-5, every gradient block within
+    1e-5 of its norm (the stated tolerance; measured <= 3.6e-6).  Ragged lengths, batches
+    that are not multiples of the 128-sequence tile, repeated indices."""
+    import torch
+    from paper_2011_14486_b200 import _lib
+    from paper_2011_14486_b200.featurizer import featurize_states, normalize
+    from paper_2011_14486_b200.trainer import DeviceGradients, flat_params
+    from paper_2011_14486_b200.value_model import load
+    g, data = _dataset(golden)
+    params = load(v0_path)
+    mats = featurize_states([s for s, _ in data])
+    T = np.array([m.shape[0] for m in mats], dtype=np.int32)
+    X = np.zeros((len(mats), T.max(), 16))
+    for i, m in enumerate(mats):
+        X[i, : len(m)] = normalize(params.normalizer, m)
+    logt = np.log([t for _, t in data])
+    dev = DeviceGradients(_lib.context(0), X, T, logt, params.hidden)
+    dev.set_params(flat_params(params))
+    H, G = 32, 128
+    blocks = {"Wx": slice(0, 16 * G), "Wh": slice(16 * G, 16 * G + H * G),
+              "b": slice(16 * G + H * G, 16 * G + H * G + G), "w": slice(16 * G + H * G + G, -1),
+              "b_out": slice(-1, None)}
+    rng = np.random.default_rng(12)
+    worst = {k: 0.0 for k in blocks}
+    for B in (1, 37, 128, 600, 4096):
+        batch = rng.integers(0, len(mats), size=B).astype(np.int32)
+        batch = batch[np.argsort(T[batch], kind="stable")]
+        out = {}
+        for mode in ("exact", "tcf"):
+            dev.set_mode(mode)
+            gb = torch.zeros(dev.n_params, dtype=torch.float64, device="cuda")
+            raw = np.zeros(B)
+            dev.grads(batch, B, params.target_scale, gb.data_ptr(), raw_out=raw)
+            dev.sync()
+            out[mode] = (raw, gb.cpu().numpy())
+        np.testing.assert_allclose(out["tcf"][0], out["exact"][0], rtol=1e-5, atol=1e-5)
+        ge, gt = out["exact"][1], out["tcf"][1]
+        for name, sl in blocks.items():
+            err = np.linalg.norm(gt[sl] - ge[sl]) / max(np.linalg.norm(ge[sl]), 1e-30)
+            worst[name] = max(worst[name], err)
+            assert err < 1e-5, (B, name, err)
+    print("tcf gradient error (norm-wise, worst over batches): " +
+          ", ".join(f"{k} {v:.1e}" for k, v in worst.items()))
+    dev.set_mode("exact")
+
+
+@pytest.mark.gpu
+def test_tensor_core_recurrences_training_run(golden, v0_path):
+    """The reference's training run in mode "tcf": the same bar as the other
+    modes - V within 1e-4 of the reference-trained v0 on the dataset (measured
+    5.4e-7) and holdout R^2 within 5e-5 of the reference's."""
+    from paper_2011_14486_b200.trainer import train
+    from paper_2011_14486_b200.value_model import TrainConfig, init_params, load, predict_states
+    g, data = _dataset(golden)
+    c = g["config"]
+    cfg = TrainConfig(c["learning_rate"], c["epochs"], c["batch_size"], c["seed"], c["clip_norm"],
+                      c["holdout_fraction"], c["patience"])
+    params, metrics = train(init_params(c["seed"], c["hidden"]), data, cfg, mode="tcf")
+    ref = load(v0_path)
+    states = [s for s, _ in data]
+    rel = np.abs(predict_states(params, states) / predict_states(ref, states) - 1)
+    print(f"tcf training: max |V/V_ref - 1| = {rel.max():.2e}, holdout R^2 {metrics['holdout_r2']:.6f} "
+          f"(reference {g['metrics']['holdout_r2']:.6f})")
+    assert abs(metrics["holdout_r2"] - g["metrics"]["holdout_r2"]) < 5e-5
+    assert rel.max() <= 1e-4, rel.max()
