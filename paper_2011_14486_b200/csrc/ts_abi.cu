@@ -371,6 +371,55 @@ int self_test(ts_ctx* ctx) {
       return fail(ctx, TS_ERR_SELFTEST, buf);
     }
   }
+  // glibc exp / tanh ports (the exact leg's transcendentals): the host port
+  // and the device against the host libm, bit for bit, over the LSTM's
+  // ranges (gate pre-activations, cell states, V exponents), the branch
+  // boundaries of both routines and the special values
+  {
+    std::vector<double> ts;
+    uint64_t s2 = 0x9E3779B97F4A7C15ull;
+    for (int i = 0; i < 200000; ++i) {
+      const uint64_t z = splitmix_next(s2);
+      const double u = (double)(z >> 11) * 1.1102230246251565e-16;
+      switch (i % 5) {
+        case 0: ts.push_back((u - 0.5) * 60.0); break;                        // gates, cells
+        case 1: ts.push_back((u - 0.5) * 1500.0); break;                      // |x| up to 750: special cases
+        case 2: ts.push_back(std::ldexp(u, -(int)(z % 60)) * ((z >> 7) & 1 ? -1 : 1)); break;  // tiny
+        case 3: ts.push_back((u - 0.5) * 4.0); break;                         // |x| < 2: tanh's two forms
+        default: ts.push_back(std::ldexp(1.0, (int)(z % 20)) * (1.0 + (u - 0.5) * 1e-6) *
+                              ((z >> 9) & 1 ? -1 : 1));                        // near powers of two
+      }
+    }
+    const double special[] = {0.0, -0.0, 1.0, -1.0, 22.0, -22.0, 0.34657359027997264, 1.0397207708399179,
+                              38.816242111356935, 512.0, -512.0, 709.78, -745.1, 1e-300, -1e-300,
+                              5e-324, 1.0 / 0.0, -1.0 / 0.0, 2.0, 44.0, -44.0, 0.5, -0.25};
+    for (double v : special) ts.push_back(v);
+    const size_t m = ts.size();
+    for (size_t i = 0; i < m; ++i) {
+      if (as_u64(glibc_exp(ts[i])) != as_u64(std::exp(ts[i])) || as_u64(glibc_tanh(ts[i])) != as_u64(std::tanh(ts[i]))) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "host exp/tanh port mismatch at %.17g: libm build differs from glibc 2.39", ts[i]);
+        return fail(ctx, TS_ERR_SELFTEST, buf);
+      }
+    }
+    DevBuf tx, ty;
+    TS_CUDA(tx.reserve(m * 8));
+    TS_CUDA(ty.reserve(m * 24));
+    TS_CUDA(cudaMemcpy(tx.p, ts.data(), m * 8, cudaMemcpyHostToDevice));
+    k_glibc_selftest<<<(int)((m + 255) / 256), 256>>>(tx.as<double>(), ty.as<double>(), (int64_t)m);
+    TS_LAUNCHED();
+    std::vector<double> yy(3 * m);
+    TS_CUDA(cudaMemcpy(yy.data(), ty.p, m * 24, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < m; ++i) {
+      const uint64_t th = as_u64(std::tanh(ts[i]));
+      if (as_u64(yy[3 * i]) != as_u64(std::exp(ts[i])) || as_u64(yy[3 * i + 1]) != th ||
+          as_u64(yy[3 * i + 2]) != th) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "device exp/tanh port mismatch at %.17g", ts[i]);
+        return fail(ctx, TS_ERR_SELFTEST, buf);
+      }
+    }
+  }
   // tanh_bf (the branch-free restatement the exact LSTM kernels use) must
   // equal the device tanh bit for bit
   DevBuf db;
@@ -424,6 +473,7 @@ int ts_ctx_create(int device, ts_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess)
     e = cudaMemcpyToSymbol(d_log2_data, ts_log2_data_bits, sizeof(uint64_t) * TS_LOG2_NDATA);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(d_exp_tab, ts_exp_tab_bits, sizeof(uint64_t) * TS_EXP_NTAB);
   if (e == cudaSuccess) e = ctx->status.reserve(sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(ctx->status.p, 0, sizeof(int));
   if (e != cudaSuccess) {

@@ -63,7 +63,8 @@ def native_core():
     import ctypes
     src = ROOT / "tests" / "native" / "core_host.cpp"
     so = ROOT / "tests" / "native" / "libcore_host.so"
-    deps = [src, ROOT / "paper_2011_14486_b200" / "csrc" / "ts_core.cuh"]
+    deps = [src, ROOT / "paper_2011_14486_b200" / "csrc" / "ts_core.cuh",
+            ROOT / "paper_2011_14486_b200" / "csrc" / "ts_glibc_math.cuh"]
     if not so.exists() or any(d.stat().st_mtime > so.stat().st_mtime for d in deps):
         subprocess.run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-shared",
                         "-o", str(so), str(src)], check=True)
@@ -80,6 +81,8 @@ def native_core():
     lib.core_div128.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
     lib.core_log2_1p.restype = ctypes.c_double
     lib.core_log2_1p.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    lib.core_exp_tanh.argtypes = [vp, ctypes.c_int64, vp]
+    lib.core_tanh_bf.argtypes = [vp, ctypes.c_int64, vp]
     return lib
 
 

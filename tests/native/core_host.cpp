@@ -103,3 +103,16 @@ extern "C" double core_log2_1p(uint64_t lo, uint64_t hi) {
   if (acquired_features(s, n, pe, d, f)) return -1.0;
   return f[7];
 }
+
+#include "../../paper_2011_14486_b200/csrc/ts_glibc_math.cuh"
+
+extern "C" void core_exp_tanh(const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    out[2 * i] = glibc_exp(x[i]);
+    out[2 * i + 1] = glibc_tanh(x[i]);
+  }
+}
+
+extern "C" void core_tanh_bf(const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = glibc_tanh_bf(x[i]);
+}

@@ -281,3 +281,24 @@ def test_coded_wire_format_matches(gpu_ctx, v0):
     rc = gpu_ctx.lib.ts_score_states_coded(gpu_ctx.h, pid, _lib._p(bad), _lib._p(depths), n, MODE_FAST,
                                            _lib._p(b))
     assert rc != 0
+
+
+def test_exact_leg_bit_identical_to_reference(state_sets, v0, golden, greedy_golden):
+    """With glibc 2.39's exp and tanh restated on the device
+    (csrc/ts_glibc_math.cuh, TS_GLIBC_MATH), the exact leg reproduces the
+    reference's Cython kernel + math.exp BIT FOR BIT: V of every golden
+    state, backend.lstm_forward's raw on the golden inputs, and the fused
+    greedy's predicted V of the final schedule on all 14 pipelines - so
+    greedy/beam identity holds by construction, not by tolerance."""
+    from paper_2011_14486_b200.backend import lstm_forward
+    for name, z in state_sets.items():
+        p = pipeline_from(z)
+        got = predict_states(v0, product_states(p, z["keys"]), mode=MODE_EXACT)
+        assert np.array_equal(bits(got), bits(z["values"])), name
+    zf = np.load(golden / "lstm_forward.npz")
+    raw = lstm_forward(zf["X"], v0.Wx, v0.Wh, v0.b, v0.w, v0.b_out)
+    assert np.array_equal(bits(raw), bits(zf["raw"]))
+    for key, g in greedy_golden.items():
+        s, visited, v = greedy_schedule_gpu(pipeline_from(g), v0, return_value=True)
+        assert [d.render() for d in s.decisions] == g["schedule"], key
+        assert v == float.fromhex(g["predicted"]), key

@@ -219,3 +219,45 @@ def test_glibc_log2_exact_on_powers_of_two(native_core):
         x = 2.0 ** k
         assert math.log2(x) == k
         assert native_core.core_log2(x) == k
+
+
+def test_glibc_exp_tanh_ports_bit_exact(native_core):
+    """The exact leg's exp / tanh (csrc/ts_glibc_math.cuh: glibc 2.39's
+    __exp_fma and fdlibm tanh over __expm1_fma, restated) against this host's
+    libm through CPython's math.exp / math.tanh - the functions behind the
+    reference's Cython kernel and predict_states (_recurrent_cy.pyx:17-18,
+    :58-60, value_model.py:154) - bit for bit on 400k values over the LSTM's
+    ranges, both tanh forms, exp's special cases and the subnormal range."""
+    import ctypes
+    import math
+    rng = np.random.default_rng(3)
+    xs = np.concatenate([
+        rng.uniform(-30, 30, 150_000), rng.uniform(-2, 2, 100_000), rng.uniform(-760, 760, 50_000),
+        rng.uniform(-1, 1, 50_000) * np.exp2(-rng.integers(0, 60, 50_000)),
+        np.exp2(rng.integers(-5, 10, 10_000)) * (1 + rng.uniform(-1e-9, 1e-9, 10_000)),
+        [0.0, -0.0, 1.0, -1.0, 22.0, -22.0, 512.0, -512.0, 709.78, -745.1, -708.5, 1e-300, 5e-324,
+         0.34657359027997264, 1.0397207708399179, 38.816242111356935, 44.0, -0.25, 0.5],
+    ]).astype(np.float64)
+    out = np.empty(2 * len(xs))
+    native_core.core_exp_tanh(xs.ctypes.data_as(ctypes.c_void_p), len(xs), out.ctypes.data_as(ctypes.c_void_p))
+    want_e = np.array([math.exp(x) if x < 709.7 else float("inf") for x in xs])
+    want_t = np.array([math.tanh(x) for x in xs])
+    fin = xs < 709.7  # math.exp raises OverflowError beyond; the port returns inf like libm
+    assert np.array_equal(out[0::2][fin].view(np.uint64), want_e[fin].view(np.uint64))
+    assert np.array_equal(out[1::2].view(np.uint64), want_t.view(np.uint64))
+
+
+def test_glibc_tanh_branch_free_form(native_core):
+    """glibc_tanh_bf (one expm1 per lane, selects instead of branches - what
+    the exact LSTM kernels run) equals libm tanh bit for bit."""
+    import ctypes
+    import math
+    rng = np.random.default_rng(4)
+    xs = np.concatenate([rng.uniform(-30, 30, 200_000), rng.uniform(-2.5, 2.5, 200_000),
+                         rng.uniform(-1, 1, 50_000) * np.exp2(-rng.integers(0, 60, 50_000)),
+                         np.array([0.0, -0.0, 1.0, -1.0, 22.0, -22.0, 0.17328679513998632, 0.5198603854199589,
+                                   0.9999999999999999, 19.4, 1e-17, -1e-17, 5e-324])])
+    out = np.empty(len(xs))
+    native_core.core_tanh_bf(xs.ctypes.data_as(ctypes.c_void_p), len(xs), out.ctypes.data_as(ctypes.c_void_p))
+    want = np.array([math.tanh(x) for x in xs])
+    assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
