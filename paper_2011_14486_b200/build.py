@@ -30,7 +30,25 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in sources())
 
 
+def build_hostenc(force: bool = False) -> pathlib.Path:
+    """The native host encoder (csrc/hostenc.c, CPython C API) in-tree."""
+    import sysconfig
+    out = HERE / ("_hostenc" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = CSRC / "hostenc.c"
+    if not force and out.exists() and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"], "-o",
+           str(out) + ".tmp", str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("gcc failed building _hostenc")
+    pathlib.Path(str(out) + ".tmp").replace(out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
+    build_hostenc(force)
     if not force and not needs_build():
         return OUT
     cmd = ["nvcc", *NVCC_FLAGS, "-o", str(OUT) + ".tmp", str(CSRC / "ts_abi.cu")]

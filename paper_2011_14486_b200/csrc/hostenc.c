@@ -1,0 +1,256 @@
+/* hostenc.c - native host-side encoding of foreign ScheduleState objects
+ * (the reference's own states, handed to the V-callable, search.py:3-8) into
+ * the 16-byte ts_decision records of the C-ABI.
+ *
+ * schedule_space.encode_states spent its time in Python per decision.  Here
+ * one C call walks a group of states: a state that already carries its
+ * records (state._cache["ts_records"], featurizer.py:72-73's cache idiom)
+ * is copied; otherwise every decision object is looked up by identity in an
+ * open-addressing table (pointer -> schedule index + record; the table holds
+ * a reference, so the pointer stays valid) and only unseen objects call back
+ * into Python (_PipelineInfo.encode: validation + encoding, cached by value
+ * there).  Search children share all but their last decision object with
+ * their parent, so a child costs one identity probe per decision.
+ *
+ * Module _hostenc (CPython C API, built in-tree by build.py):
+ *   encode_group(states, idxs, T, fallback) -> (records: bytes, offsets: bytes [int64 n+1])
+ *   clear() -> None   (drop the identity table)
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <string.h>
+
+typedef struct {
+  PyObject* obj; /* strong reference; NULL = empty slot */
+  int32_t idx;
+  uint8_t rec[16];
+} Slot;
+
+#define CAP_LOG2 20
+#define CAP (1u << CAP_LOG2)
+static Slot* table = NULL;
+static size_t used = 0;
+static PyObject* s_cache = NULL;   /* "_cache" */
+static PyObject* s_records = NULL; /* "ts_records" */
+static PyObject* s_decisions = NULL;
+
+static void table_clear(void) {
+  if (!table) return;
+  for (size_t i = 0; i < CAP; ++i) {
+    if (table[i].obj) {
+      Py_DECREF(table[i].obj);
+      table[i].obj = NULL;
+    }
+  }
+  used = 0;
+}
+
+static inline size_t slot_of(const void* p) {
+  uint64_t h = (uint64_t)(uintptr_t)p;
+  h ^= h >> 33;
+  h *= 0xff51afd7ed558ccdull;
+  h ^= h >> 33;
+  return (size_t)(h & (CAP - 1));
+}
+
+/* record of decision d at schedule index j: table hit or Python fallback */
+static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
+  size_t s = slot_of(d);
+  for (;;) {
+    Slot* e = &table[s];
+    if (!e->obj) break;
+    if (e->obj == d && e->idx == j) {
+      memcpy(out, e->rec, 16);
+      return 0;
+    }
+    s = (s + 1) & (CAP - 1);
+  }
+  PyObject* jj = PyLong_FromLong(j); /* a cached small int */
+  if (!jj) return -1;
+  PyObject* argv[2] = {jj, d};
+  PyObject* r = PyObject_Vectorcall(fallback, argv, 2, NULL);
+  Py_DECREF(jj);
+  if (!r) return -1;
+  if (!PyBytes_Check(r) || PyBytes_GET_SIZE(r) != 16) {
+    Py_DECREF(r);
+    PyErr_SetString(PyExc_TypeError, "encode fallback must return 16 bytes");
+    return -1;
+  }
+  memcpy(out, PyBytes_AS_STRING(r), 16);
+  Py_DECREF(r);
+  if (used >= CAP / 2) table_clear(); /* bounded: foreign callers bring new objects */
+  s = slot_of(d);
+  while (table[s].obj) s = (s + 1) & (CAP - 1);
+  Py_INCREF(d);
+  table[s].obj = d;
+  table[s].idx = j;
+  memcpy(table[s].rec, out, 16);
+  ++used;
+  return 0;
+}
+
+static PyObject* encode_group(PyObject* self, PyObject* args) {
+  (void)self;
+  PyObject *states, *idxs, *fallback;
+  Py_ssize_t T;
+  if (!PyArg_ParseTuple(args, "OOnO", &states, &idxs, &T, &fallback)) return NULL;
+  if (!table) {
+    table = (Slot*)PyMem_Calloc(CAP, sizeof(Slot));
+    if (!table) return PyErr_NoMemory();
+  }
+  PyObject* sq = PySequence_Fast(states, "states must be a sequence");
+  if (!sq) return NULL;
+  PyObject* iq = PySequence_Fast(idxs, "indices must be a sequence");
+  if (!iq) {
+    Py_DECREF(sq);
+    return NULL;
+  }
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(iq);
+  PyObject* offs = PyBytes_FromStringAndSize(NULL, (n + 1) * (Py_ssize_t)sizeof(int64_t));
+  Py_ssize_t cap = n * 20 + 16, len = 0;
+  uint8_t* buf = (uint8_t*)PyMem_Malloc((size_t)cap * 16);
+  if (!offs || !buf) {
+    Py_XDECREF(offs);
+    PyMem_Free(buf);
+    Py_DECREF(sq);
+    Py_DECREF(iq);
+    return PyErr_NoMemory();
+  }
+  int64_t* off = (int64_t*)PyBytes_AS_STRING(offs);
+  off[0] = 0;
+  PyObject* const* sv = PySequence_Fast_ITEMS(sq);
+  const Py_ssize_t ns = PySequence_Fast_GET_SIZE(sq);
+  for (Py_ssize_t q = 0; q < n; ++q) {
+    const Py_ssize_t i = PyLong_AsSsize_t(PySequence_Fast_GET_ITEM(iq, q));
+    if (i < 0 || i >= ns) {
+      if (!PyErr_Occurred()) PyErr_SetString(PyExc_IndexError, "state index out of range");
+      goto fail;
+    }
+    PyObject* st = sv[i];
+    /* a state carrying its records (state._cache["ts_records"]) */
+    PyObject* cache = PyObject_GetAttr(st, s_cache);
+    if (!cache) PyErr_Clear();
+    if (cache && PyDict_Check(cache)) {
+      PyObject* hit = PyDict_GetItemWithError(cache, s_records); /* borrowed */
+      if (hit && PyBytes_Check(hit) && PyBytes_GET_SIZE(hit) % 16 == 0) {
+        const Py_ssize_t m = PyBytes_GET_SIZE(hit) / 16;
+        if (m > T) {
+          Py_DECREF(cache);
+          PyErr_SetString(PyExc_ValueError, "state has more decisions than stages");
+          goto fail;
+        }
+        if (len + m > cap) {
+          cap = 2 * (len + m) + 16;
+          uint8_t* nb = (uint8_t*)PyMem_Realloc(buf, (size_t)cap * 16);
+          if (!nb) {
+            Py_DECREF(cache);
+            PyErr_NoMemory();
+            goto fail;
+          }
+          buf = nb;
+        }
+        memcpy(buf + len * 16, PyBytes_AS_STRING(hit), (size_t)m * 16);
+        len += m;
+        off[q + 1] = len;
+        Py_DECREF(cache);
+        continue;
+      }
+      if (PyErr_Occurred()) {
+        Py_DECREF(cache);
+        goto fail;
+      }
+    }
+    PyObject* dec = PyObject_GetAttr(st, s_decisions);
+    if (!dec) {
+      Py_XDECREF(cache);
+      goto fail;
+    }
+    PyObject* dq = PySequence_Fast(dec, "decisions must be a sequence");
+    Py_DECREF(dec);
+    if (!dq) {
+      Py_XDECREF(cache);
+      goto fail;
+    }
+    const Py_ssize_t m = PySequence_Fast_GET_SIZE(dq);
+    if (m > T) {
+      Py_DECREF(dq);
+      Py_XDECREF(cache);
+      PyErr_SetString(PyExc_ValueError, "state has more decisions than stages");
+      goto fail;
+    }
+    if (len + m > cap) {
+      cap = 2 * (len + m) + 16;
+      uint8_t* nb = (uint8_t*)PyMem_Realloc(buf, (size_t)cap * 16);
+      if (!nb) {
+        Py_DECREF(dq);
+        Py_XDECREF(cache);
+        PyErr_NoMemory();
+        goto fail;
+      }
+      buf = nb;
+    }
+    PyObject* const* dv = PySequence_Fast_ITEMS(dq);
+    for (Py_ssize_t j = 0; j < m; ++j) {
+      if (record_of(dv[j], (int)j, fallback, buf + (len + j) * 16)) {
+        Py_DECREF(dq);
+        Py_XDECREF(cache);
+        goto fail;
+      }
+    }
+    if (cache && PyDict_Check(cache)) { /* cache the records on the state, like records_of */
+      PyObject* rb = PyBytes_FromStringAndSize((const char*)(buf + len * 16), m * 16);
+      if (!rb || PyDict_SetItem(cache, s_records, rb) < 0) {
+        Py_XDECREF(rb);
+        Py_DECREF(dq);
+        Py_DECREF(cache);
+        goto fail;
+      }
+      Py_DECREF(rb);
+    }
+    Py_XDECREF(cache);
+    Py_DECREF(dq);
+    len += m;
+    off[q + 1] = len;
+  }
+  Py_DECREF(sq);
+  Py_DECREF(iq);
+  PyObject* recs = PyBytes_FromStringAndSize((const char*)buf, len * 16);
+  PyMem_Free(buf);
+  if (!recs) {
+    Py_DECREF(offs);
+    return NULL;
+  }
+  PyObject* res = PyTuple_Pack(2, recs, offs);
+  Py_DECREF(recs);
+  Py_DECREF(offs);
+  return res;
+fail:
+  Py_DECREF(sq);
+  Py_DECREF(iq);
+  Py_DECREF(offs);
+  PyMem_Free(buf);
+  return NULL;
+}
+
+static PyObject* clear(PyObject* self, PyObject* args) {
+  (void)self;
+  (void)args;
+  table_clear();
+  Py_RETURN_NONE;
+}
+
+static PyMethodDef methods[] = {
+    {"encode_group", encode_group, METH_VARARGS, "records + offsets of states[idxs] (see hostenc.c)"},
+    {"clear", clear, METH_NOARGS, "drop the decision identity table"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_hostenc", NULL, -1, methods};
+
+PyMODINIT_FUNC PyInit__hostenc(void) {
+  s_cache = PyUnicode_InternFromString("_cache");
+  s_records = PyUnicode_InternFromString("ts_records");
+  s_decisions = PyUnicode_InternFromString("decisions");
+  if (!s_cache || !s_records || !s_decisions) return NULL;
+  return PyModule_Create(&module);
+}

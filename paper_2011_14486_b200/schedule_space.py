@@ -11,6 +11,7 @@ Candidate enumeration and legality run in the native library
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -23,6 +24,7 @@ SPLIT_FACTORS = (8, 32)  # schedule_space.py:28-30
 VEC_WIDTHS = (1, 8)
 MAX_COMPUTE_AT_LEVELS = 3
 FLAG_PARALLEL, FLAG_STORE_AT = 1, 2
+_REC = struct.Struct("<4B8B3Bb")  # ts_decision: split[4], order[8], n_loops, vec, flags, anchor
 
 
 @dataclass(frozen=True)
@@ -150,18 +152,29 @@ class _PipelineInfo:
         if hit is not None and hit[0] is d and hit[2] == idx:  # a record is only valid at its stage
             return hit[1]
         try:
-            b = self.val_cache.get((idx, d))
-        except TypeError:  # an unhashable decision-like object
-            b = None
-        if b is not None:
-            return b
+            key = (idx, d.stage, d.splits, d.order, d.vectorize_width, d.parallel, d.compute_at,
+                   d.store_at)
+            b = self.val_cache.get(key)
+        except (TypeError, AttributeError):  # an unhashable or incomplete decision-like object
+            key, b = None, None
+        if b is None:
+            b = self._encode_fields(idx, d)
+            if key is not None and len(self.val_cache) < (1 << 20):
+                self.val_cache[key] = b
+        if len(self.enc_cache) >= (1 << 20):  # bounded: foreign callers bring new objects
+            self.enc_cache.clear()
+        self.enc_cache[id(d)] = (d, b, idx)
+        return b
+
+    def _encode_fields(self, idx: int, d) -> bytes:
+        """The 16-byte ts_decision of decision d at schedule index idx."""
         st = self.stages[idx]
         if d.stage != st.name:
             raise IllegalActionError(
                 f"expected a decision for stage {st.name!r}, got {d.stage!r}")
-        rec = np.zeros(1, _lib.DECISION_DTYPE)[0]
         pure = [n for n, _ in st.dims]
         split = {}
+        sp = [0, 0, 0, 0]
         for dim, f in d.splits:
             if dim in split:
                 raise IllegalActionError(f"{st.name}: dim {dim} split twice")
@@ -172,21 +185,17 @@ class _PipelineInfo:
             if f > 255:
                 raise PipelineError(f"{st.name}: split factor {f} outside the record envelope")
             split[dim] = f
-            rec["split"][pure.index(dim)] = f
+            sp[pure.index(dim)] = f
         table = self.loop_table(st, split)
         if sorted(d.order) != sorted(table) or len(d.order) > 8:
             raise IllegalActionError(
                 f"{st.name}: order {d.order} is not a permutation of loops {sorted(table)}")
-        rec["order"][:] = 0xFF
-        for j, name in enumerate(d.order):
-            rec["order"][j] = table[name]
-        rec["n_loops"] = len(d.order)
+        order = [table[name] for name in d.order] + [0xFF] * (8 - len(d.order))
         if not 1 <= d.vectorize_width <= 255:
             raise IllegalActionError(f"{st.name}: bad vectorize width {d.vectorize_width}")
-        rec["vec"] = d.vectorize_width
         flags = FLAG_PARALLEL if d.parallel else 0
         if d.compute_at is None:
-            rec["anchor"] = -1
+            anchor = -1
             if d.store_at is not None:
                 raise IllegalActionError(f"{st.name}: store_at must be Root or the compute_at site")
         else:
@@ -197,23 +206,13 @@ class _PipelineInfo:
                     f"{st.name}: compute_at target must be the sole consumer (consumers: {cons})")
             if not 0 <= lvl < 8:
                 raise IllegalActionError(f"{st.name}: loop level {lvl} does not exist in {cname}'s nest")
-            rec["anchor"] = lvl
+            anchor = lvl
             if d.store_at is not None:
                 if d.store_at != d.compute_at:
                     raise IllegalActionError(
                         f"{st.name}: store_at must be Root or the compute_at site")
                 flags |= FLAG_STORE_AT
-        rec["flags"] = flags
-        b = rec.tobytes()
-        if len(self.enc_cache) >= (1 << 20):  # bounded: foreign callers bring new objects
-            self.enc_cache.clear()
-        self.enc_cache[id(d)] = (d, b, idx)
-        try:
-            if len(self.val_cache) < (1 << 20):
-                self.val_cache[(idx, d)] = b
-        except TypeError:
-            pass
-        return b
+        return _REC.pack(*sp, *order, len(d.order), d.vectorize_width, flags, anchor)
 
     def decode(self, idx: int, rec) -> LayerSchedule:
         st = self.stages[idx]
@@ -244,21 +243,32 @@ class _PipelineInfo:
         return out
 
 
+try:  # the native host encoder (built in-tree by build.py)
+    from . import _hostenc
+except ImportError:  # not built: the Python path below (host-only, same records)
+    _hostenc = None
+
 _INFO: dict = {}
+_INFO_ID: dict = {}  # id(pipeline) -> (pipeline, info): no hashing of the object
 
 
 def _info(p) -> _PipelineInfo:
-    # per-object cache first: hashing a Pipeline walks every stage
+    # identity first: hashing a Pipeline (a frozen dataclass in the
+    # reference) walks every stage, ~0.3 ms for VGG-16
+    hit = _INFO_ID.get(id(p))
+    if hit is not None and hit[0] is p:
+        return hit[1]
     cache = getattr(p, "_cache", None)
-    if isinstance(cache, dict):
-        inf = cache.get("ts_info")
-        if inf is not None:
-            return inf
-    inf = _INFO.get(p)
+    inf = cache.get("ts_info") if isinstance(cache, dict) else None
     if inf is None:
-        inf = _INFO[p] = _PipelineInfo(p)
-    if isinstance(cache, dict):
-        cache["ts_info"] = inf
+        inf = _INFO.get(p)
+        if inf is None:
+            inf = _INFO[p] = _PipelineInfo(p)
+        if isinstance(cache, dict):
+            cache["ts_info"] = inf
+    if len(_INFO_ID) > 4096:
+        _INFO_ID.clear()
+    _INFO_ID[id(p)] = (p, inf)  # the strong reference keeps the id valid
     return inf
 
 
@@ -266,10 +276,23 @@ def encode_states(states):
     """Group states by pipeline -> [(pipeline_info, indices, records, offsets)]."""
     groups = {}
     for i, s in enumerate(states):
-        groups.setdefault(s.pipeline, []).append(i)
+        p = s.pipeline
+        g = groups.get(id(p))
+        if g is None:
+            g = groups[id(p)] = (p, [])
+        g[1].append(i)
     out = []
-    for p, idxs in groups.items():
+    for p, idxs in groups.values():
         inf = _info(p)
+        if _hostenc is not None:  # native: one C call per group (csrc/hostenc.c)
+            try:
+                rb, ob = _hostenc.encode_group(states, idxs, inf.T, inf.encode)
+            except ValueError as e:
+                raise IllegalActionError(str(e)) from None
+            recs = np.frombuffer(rb, dtype=_lib.DECISION_DTYPE)
+            offsets = np.frombuffer(ob, dtype=np.int64)
+            out.append((inf, idxs, recs, offsets))
+            continue
         chunks = [inf.records_of(states[i]) for i in idxs]
         lens = np.fromiter((len(c) // 16 for c in chunks), dtype=np.int64, count=len(chunks))
         if np.any(lens > inf.T):

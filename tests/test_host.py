@@ -261,3 +261,35 @@ def test_glibc_tanh_branch_free_form(native_core):
     native_core.core_tanh_bf(xs.ctypes.data_as(ctypes.c_void_p), len(xs), out.ctypes.data_as(ctypes.c_void_p))
     want = np.array([math.tanh(x) for x in xs])
     assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
+
+
+def test_native_host_encoder_matches_python_path(greedy_golden):
+    """csrc/hostenc.c (identity-cached decision records, one C call per
+    pipeline group) returns exactly the Python path's records and offsets, on
+    states sharing decision objects (search children), on repeated state
+    objects, and raises the same errors."""
+    assert ss._hostenc is not None, "the native host encoder is not built"
+    ss._hostenc.clear()
+    g = greedy_golden["assets/pipelines/nets/vgg16.pl"]
+    p = pi.parse_pipeline(g["text"])
+    s = ss.initial_state(p)
+    states = []
+    for k, r in enumerate(g["schedule"]):
+        cands = ss.candidate_actions(s)
+        states.extend(ss.child_state(s, a) for a in cands[:5])  # children share the parent's objects
+        s = ss.apply(s, ss.parse_layer_schedule(r))
+    states += states[:7]  # repeated objects
+    native = ss.encode_states(states)
+    saved, ss._hostenc = ss._hostenc, None
+    try:
+        for st in states:
+            st._cache.pop("ts_records", None)
+        python = ss.encode_states(states)
+    finally:
+        ss._hostenc = saved
+    assert len(native) == len(python) == 1
+    assert np.array_equal(native[0][2].view(np.uint8), python[0][2].view(np.uint8))
+    assert np.array_equal(native[0][3], python[0][3])
+    bad = ss.ScheduleState(p, tuple(ss.initial_state(p).decisions) + (ss.LayerSchedule("nope", (), ("x",)),))
+    with pytest.raises(IllegalActionError):
+        ss.encode_states([bad])
