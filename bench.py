@@ -460,6 +460,54 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
             "targets": "device cost oracle (cost_oracle.benchmark) of each prefix's schedule"}
 
 
+# --------------------------------------------------------------- level 1: the V-callable
+def v_callable_rate(params_path, seed=77):
+    """INTEGRATION.md level 1: the reference's own ScheduleState objects scored
+    through this package's V-callable (search.model_value, the seam of
+    search.py:3-8).  The states are the reference's children along one VGG-16
+    walk (apply(s, a) for every candidate of every layer: search-shaped, each
+    child shares its parent's decision objects), built untimed by the
+    reference; timed: V(children) - host encoding (csrc/hostenc.c) + device
+    scoring + results - next to the reference's own model_value on the same
+    objects (Cython, one process)."""
+    _ref_import()
+    from tensched.pipeline_ir import parse_pipeline
+    from tensched.schedule_space import apply, candidate_actions, initial_state
+    from tensched.search import SearchRng
+    from tensched.search import model_value as ref_model_value
+    from tensched.value_model import load as ref_load
+    from paper_2011_14486_b200.search import model_value
+    params = ref_load(str(params_path))
+    p = parse_pipeline(VGG.read_text())
+
+    def children_of_walk():
+        rng = SearchRng(seed)
+        s = initial_state(p)
+        out = []
+        while not s.is_complete:
+            c = candidate_actions(s)
+            out.extend(apply(s, a) for a in c)
+            s = apply(s, c[rng.randrange(len(c))])
+        return out
+    V = model_value(params)
+    V(children_of_walk()[:64])  # warm: pipeline descriptor, context
+    kids = children_of_walk()
+    t0 = time.perf_counter()
+    v = V(kids)
+    dt = time.perf_counter() - t0
+    ref_kids = children_of_walk()
+    t0 = time.perf_counter()
+    rv = ref_model_value(params)(ref_kids)
+    rdt = time.perf_counter() - t0
+    import numpy as np
+    same = bool(np.array_equal(np.asarray(v, dtype=np.float64).view(np.uint64),
+                               np.asarray(rv, dtype=np.float64).view(np.uint64)))
+    return {"states": len(kids), "value": len(kids) / dt, "unit": "states/s",
+            "reference_1proc": len(ref_kids) / rdt, "bitwise_equal_to_reference": same,
+            "note": "fresh reference ScheduleState children of one VGG-16 walk, V(children) through "
+                    "search.model_value (exact leg) vs tensched.search.model_value (Cython)"}
+
+
 # --------------------------------------------------------------- 1e8 states, one GPU
 def big_sweep(ctx, pid, T, n_big, shard, mode, dev, stream, ref_out):
     """BASELINE configs[3]'s largest point on ONE GPU: n_big random partial
@@ -792,7 +840,7 @@ def main():
     if not args.no_train:
         train_line = train_throughput(ctx, pid, inf, params, rank, world, dev, args)
 
-    greedy, beam = {}, {}
+    greedy, beam, level1 = {}, {}, None
     if rank == 0 and not args.no_greedy:
         from paper_2011_14486_b200.search import greedy_schedule_gpu
         for net in ("crp2d", "resnet18", "resnet50", "mobilenet_v2"):
@@ -821,6 +869,10 @@ def main():
             s = beam_search_gpu(initial_state(pn), params, 8)
             beam[net] = {"wall_s": round(time.perf_counter() - t0, 4), "first_call_s": round(first, 4),
                          "width": 8, "schedule": [d.render() for d in s.decisions]}
+        try:
+            level1 = v_callable_rate(GOLD / "v0.ckpt")
+        except Exception as e:  # reported, never silently replaced
+            level1 = {"unavailable": str(e)}
         if not args.no_ref_greedy:
             try:
                 tasks = [("greedy", n) for n in greedy] + [("beam", n) for n in beam]
@@ -880,6 +932,7 @@ def main():
             "cpu_baseline": cpu,
             "greedy_wall_s": greedy,
             "beam_wall_s": beam,
+            "v_callable_reference_states": level1,
             "sweep_states_per_s": sweep,
             "exact_leg": exact_leg,
             "sweep_1e8_one_gpu": big,

@@ -134,28 +134,18 @@ __device__ __forceinline__ float sigm_s(float u) { return tc::rcp(1.0f + tc::ex2
 __device__ __forceinline__ float tanh_s(float v) { return fmaf(2.0f, tc::rcp(1.0f + tc::ex2(v)), -1.0f); }  // v = -2log2e z
 constexpr float C2 = -2.0f * tc::LOG2E;
 
-// x of row (sequence) at timestep t as floats
-__device__ __forceinline__ void row_x(const tr::Data& D, int idx, int T, int d, int t, float* x) {
-  const double* src = t < T - d ? D.init + (int64_t)(D.init_base[idx] + t) * 16
-                                : D.rows + (D.row_base[idx] + (T - 1 - t)) * 16;
-#pragma unroll
-  for (int k = 0; k < 16; k += 2) {
-    const double2 v = __ldg(reinterpret_cast<const double2*>(src + k));
-    x[k] = (float)v.x;
-    x[k + 1] = (float)v.y;
-  }
+// x of row (sequence) at timestep t, raw f64 pairs: loads issued as a
+// prefetch and converted only where used (converting at the load would
+// stall on it right there)
+__device__ __forceinline__ const double* row_src(const tr::Data& D, int idx, int T, int d, int t) {
+  return t < T - d ? D.init + (int64_t)(D.init_base[idx] + t) * 16 : D.rows + (D.row_base[idx] + (T - 1 - t)) * 16;
 }
 
-// 4 features of row x (features 4 q .. 4 q + 3) as floats
-__device__ __forceinline__ void row_x4(const tr::Data& D, int idx, int T, int d, int t, int q, float* x) {
-  const double* src = t < T - d ? D.init + (int64_t)(D.init_base[idx] + t) * 16
-                                : D.rows + (D.row_base[idx] + (T - 1 - t)) * 16;
-  const double2 v0 = __ldg(reinterpret_cast<const double2*>(src + 4 * q));
-  const double2 v1 = __ldg(reinterpret_cast<const double2*>(src + 4 * q + 2));
-  x[0] = (float)v0.x;
-  x[1] = (float)v0.y;
-  x[2] = (float)v1.x;
-  x[3] = (float)v1.y;
+// 4 features of row x (features 4 q .. 4 q + 3)
+__device__ __forceinline__ void row_x4(const tr::Data& D, int idx, int T, int d, int t, int q, double2* x) {
+  const double2* src = reinterpret_cast<const double2*>(row_src(D, idx, T, d, t) + 4 * q);
+  x[0] = __ldg(src);
+  x[1] = __ldg(src + 1);
 }
 
 // 4 floats -> split fp16 half-chunks (8 bytes each), hi at p, lo at p + lo_off
@@ -236,21 +226,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_trc_fwd(Args a) {
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const uint32_t a_base = tc::smem_u32(A), b_base = tc::smem_u32(Bw);
   uint32_t phase = 0;
-  float x[16];
-  if (wg == 0 && T > 0) row_x(a.D, idx, T, d, 0, x);
+  double2 x[2];  // features 4 g8 .. 4 g8 + 3 of x_t: each warpgroup writes a quarter of A's x part
+  if (T > 0) row_x4(a.D, idx, T, d, 0, g8, x);
+  uint8_t* xq = A + (g8 >> 1) * tc::CHUNK_STRIDE + (r >> 3) * 128 + (r & 7) * 16 + (g8 & 1) * 8;
   for (int t = 0; t < a.Tmax; ++t) {
     const bool act = t < T;
-    if (wg == 0) {  // x part of A (rows past their length feed zeros; their results are unused)
-      float xz[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) xz[k] = act ? x[k] : 0.0f;
-      uint4 hi, lo;
-      split8(xz, hi, lo);
-      tc::st_chunk(A, 0, r, hi);
-      tc::st_chunk(A, 6, r, lo);
-      split8(xz + 8, hi, lo);
-      tc::st_chunk(A, 1, r, hi);
-      tc::st_chunk(A, 7, r, lo);
+    {  // rows past their length feed zeros; their results are unused
+      const float xz[4] = {act ? (float)x[0].x : 0.0f, act ? (float)x[0].y : 0.0f, act ? (float)x[1].x : 0.0f,
+                           act ? (float)x[1].y : 0.0f};
+      st_split4(xq, 6 * tc::CHUNK_STRIDE, xz);  // hi in chunk g8 / 2, lo in chunk 6 + g8 / 2
     }
     tc::fence_async_smem();
     tc::fence_before();
@@ -263,7 +247,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_trc_fwd(Args a) {
                     tc::umma_desc(b_base + s * 2 * tc::CHUNK_STRIDE, tc::CHUNK_STRIDE, 128), s > 0);
       tc::mma_commit(bar);
     }
-    if (wg == 0 && t + 1 < T) row_x(a.D, idx, T, d, t + 1, x);  // next row in flight across the UMMA
+    if (t + 1 < T) row_x4(a.D, idx, T, d, t + 1, g8, x);  // next row in flight across the UMMA
     tc::mbar_wait(bar, phase);
     phase ^= 1u;
     tc::fence_after();
@@ -430,6 +414,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
   const uint32_t lane_dh = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const uint32_t dz_base = tc::smem_u32(dzb), xh_base = tc::smem_u32(xhb), wt_base = tc::smem_u32(wtb);
   const uint32_t t_dh = tmem, t_dw = tmem + 64;
+  // UMMA descriptor bases: (a) dz K-major [hi, lo], Wh^T [hi, lo];
+  // (b) dz MN-major [hi, lo], [x | h | 1] MN-major [hi, lo]
+  const uint64_t dA[2] = {tc::umma_desc(dz_base, 2048, 128), tc::umma_desc(dz_base + DZ_BYTES, 2048, 128)};
+  const uint64_t dW[2] = {tc::umma_desc(wt_base, WT_CS, 128), tc::umma_desc(wt_base + WT_BYTES, WT_CS, 128)};
+  const uint64_t dB[2] = {tc::umma_desc(dz_base, 128, 2048), tc::umma_desc(dz_base + DZ_BYTES, 128, 2048)};
+  const uint64_t dX[2] = {tc::umma_desc(xh_base, 128, 2048), tc::umma_desc(xh_base + XH_BYTES, 128, 2048)};
   float dcn[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) dcn[u] = 0.0f;
@@ -438,7 +428,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
   for (int u = 0; u < 8; ++u) wj[u] = wsh[g8 * 8 + u];
   uint32_t phase = 0;
   Rec q;
-  float x[4];  // features 4 g8 .. 4 g8 + 3 of x_t (each warpgroup writes a quarter of x)
+  double2 x[2];  // features 4 g8 .. 4 g8 + 3 of x_t (each warpgroup writes a quarter of x)
   {
     const int t0 = a.Tmax - 1;
     if (t0 < T) {
@@ -483,9 +473,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
     st_split8(dzb + op_off(12 + g8, r), DZ_BYTES, zo);
     st_split8(xhb + op_off(2 + g8, r), XH_BYTES, hp);
     {  // a quarter of x_t (features 4 g8 ..), and the ones column (db) / zero padding
-      float xz[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) xz[k] = act ? x[k] : 0.0f;
+      const float xz[4] = {act ? (float)x[0].x : 0.0f, act ? (float)x[0].y : 0.0f, act ? (float)x[1].x : 0.0f,
+                           act ? (float)x[1].y : 0.0f};
       st_split4(xhb + op_off(g8 >> 1, r) + (g8 & 1) * 8, XH_BYTES, xz);
       if (g8 < 2) {
         const float one[4] = {(act && g8 == 0) ? 1.0f : 0.0f, 0, 0, 0};
@@ -505,25 +494,24 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
+      // descriptors: the operand addresses are fixed, so each UMMA's pair is
+      // a loop-invariant base plus a constant (the address field is addr >> 4)
 #pragma unroll
       for (int p = 0; p < 3; ++p) {  // hi.hi, lo.hi, hi.lo
-        const uint32_t da = dz_base + (p == 1 ? DZ_BYTES : 0);
-        const uint32_t dwh = wt_base + (p == 2 ? WT_BYTES : 0);
+        const uint64_t da = dA[p == 1], dw = dW[p == 2];
 #pragma unroll
-        for (int s = 0; s < G / 16; ++s) {
+        for (int s = 0; s < G / 16; ++s)
           // (a) S dh_next[rows x 32] = dz[rows x gates] . Wh^T: K = gates 16s..16s+15
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(t_dh),
-              "l"(tc::umma_desc(da + s * 2 * 2048, 2048, 128)), "l"(tc::umma_desc(dwh + s * 2 * WT_CS, WT_CS, 128)),
-              "r"(IDESC_DH), "r"((p > 0 || s > 0) ? 1u : 0u)
+              "l"(da + (uint64_t)(s * 2 * 2048 >> 4)), "l"(dw + (uint64_t)(s * 2 * WT_CS >> 4)), "r"(IDESC_DH),
+              "r"((p > 0 || s > 0) ? 1u : 0u)
               : "memory");
-        }
       }
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
-        const uint32_t da = dz_base + (p == 1 ? DZ_BYTES : 0);
-        const uint32_t dxh = xh_base + (p == 2 ? XH_BYTES : 0);
+        const uint64_t da = dB[p == 1], dx = dX[p == 2];
 #pragma unroll
         for (int s = 0; s < TM / 16; ++s) {
           // (b) S dW^T[gates x 64] += dz^T[gates x rows] . [x|h|1][rows x 64]: K = rows 16s..16s+15
@@ -532,8 +520,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(t_dw),
-              "l"(tc::umma_desc(da + s * 256, 128, 2048)), "l"(tc::umma_desc(dxh + s * 256, 128, 2048)),
-              "r"(IDESC_WG), "r"(accum ? 1u : 0u)
+              "l"(da + (uint64_t)(s * 256 >> 4)), "l"(dx + (uint64_t)(s * 256 >> 4)), "r"(IDESC_WG),
+              "r"(accum ? 1u : 0u)
               : "memory");
         }
       }
