@@ -19,6 +19,9 @@
  *   ts_candidates          <- schedule_space.candidate_actions (schedule_space.py:379-452)
  *   ts_greedy              <- search.greedy_schedule (search.py:90-112), fused:
  *                             candidates -> featurize -> V -> (noise) -> argmin per layer
+ *   ts_beam                <- search.beam_search (search.py:115-133), fused per layer
+ *   ts_score_children      <- one layer step of greedy_schedule for any parent (search.py:97-110)
+ *   ts_train_*             <- value_model.gradients / train (value_model.py:182-293)
  *   ts_params_upload       <- value_model.ValueModelParams / load (value_model.py:37-70, :332-376)
  *   ts_pipeline_upload     <- pipeline_ir.Pipeline (pipeline_ir.py:116-161) as a flat descriptor
  *
