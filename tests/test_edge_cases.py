@@ -159,3 +159,37 @@ def test_round_config_rejects_zero_schedules():
     with pytest.raises(PipelineError):
         RoundConfig(schedules_per_pipeline=0)
     assert RoundConfig(schedules_per_pipeline=1).schedules_per_pipeline == 1
+
+
+@pytest.mark.gpu
+def test_beam_rejects_illegal_prefix(v0_path, greedy_golden):
+    from paper_2011_14486_b200.search import beam_search_gpu
+    from paper_2011_14486_b200.value_model import load
+    params = load(v0_path)
+    g = greedy_golden["ref:pipelines/toys/t3_chain.pl"]
+    p = pipeline_from(g)
+    # a compute_at level the consumer's nest does not have
+    bad = ss.ScheduleState(p, (ss.parse_layer_schedule(g["schedule"][0]),
+                               ss.LayerSchedule("relu", (), ("x",), 1, False, ("pool", 7), None)))
+    with pytest.raises((IllegalActionError, PipelineError)):
+        beam_search_gpu(bad, params, 4)
+
+
+@pytest.mark.gpu
+def test_backend_backward_edge_cases(v0_path):
+    """Empty batch, a single timestep, and a cache from another batch."""
+    from paper_2011_14486_b200 import backend
+    from paper_2011_14486_b200.value_model import load
+    p = load(v0_path)
+    X0 = np.zeros((0, 5, 16))
+    raw, cache = backend.lstm_forward_cached(X0, p.Wx, p.Wh, p.b, p.w, p.b_out)
+    assert raw.shape == (0,)
+    g = backend.lstm_backward(X0, p.Wx, p.Wh, p.w, cache, np.zeros(0))
+    assert all(np.all(np.asarray(x) == 0) for x in g)
+    X1 = np.random.default_rng(0).normal(size=(3, 1, 16))
+    raw, cache = backend.lstm_forward_cached(X1, p.Wx, p.Wh, p.b, p.w, p.b_out)
+    dWx, dWh, db, dw, db_out = backend.lstm_backward(X1, p.Wx, p.Wh, p.w, cache, np.ones(3))
+    assert np.all(dWh == 0)  # h_{-1} = 0: no recurrent gradient with one timestep
+    assert db_out == 3.0
+    with pytest.raises(ValueError):
+        backend.lstm_backward(X1 + 1.0, p.Wx, p.Wh, p.w, cache, np.ones(3))
