@@ -71,6 +71,8 @@ def parse_args():
     ap.add_argument("--no-ref-greedy", action="store_true",
                     help="skip timing the reference's greedy_schedule on this host")
     ap.add_argument("--no-exact", action="store_true", help="skip the fp64 leg's sweep rate")
+    ap.add_argument("--device-format", default="records", choices=["records", "codes"],
+                    help="device-resident input format of the timed sweep")
     return ap.parse_args()
 
 
@@ -640,9 +642,20 @@ def main():
     out = torch.empty(M, dtype=torch.float64, device=dev)
     stream = torch.cuda.ExternalStream(ctx.lib.ts_stream(ctx.h), device=dev)
 
+    # device-resident wire format: 16-bit action codes (2 B per decision,
+    # decoded through the L2-resident code table) or the 16-byte records
+    d_codes = torch.empty(max(n_records, 1), dtype=torch.int16, device=dev)
+    ctx.check(ctx.lib.ts_encode_codes_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M, d_codes.data_ptr()))
+    dev_fmt = args.device_format
+
     def step():
-        ctx.check(ctx.lib.ts_score_states_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M,
-                                                 n_records, mode, out.data_ptr()))
+        if dev_fmt == "codes":
+            ctx.check(ctx.lib.ts_score_states_coded_device(ctx.h, pid, d_codes.data_ptr(), offs.data_ptr(), M,
+                                                           n_records if mode != _lib.MODE_FAST else n_records,
+                                                           mode, out.data_ptr()))
+        else:
+            ctx.check(ctx.lib.ts_score_states_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M,
+                                                     n_records, mode, out.data_ptr()))
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -688,8 +701,6 @@ def main():
     # codes (ts_score_states_coded), every decision of these walks being in
     # candidate_actions' space; prepared outside the timed region (encoded
     # on the device here, as schedule_space.action_codes does on the host)
-    d_codes = torch.empty(max(n_records, 1), dtype=torch.int16, device=dev)
-    ctx.check(ctx.lib.ts_encode_codes_device(ctx.h, pid, recs.data_ptr(), offs.data_ptr(), M, d_codes.data_ptr()))
     h_wire = torch.empty(n_records, dtype=torch.int16, pin_memory=True)
     h_wire.copy_(d_codes[:n_records])
     h_depth = torch.empty(M, dtype=torch.uint8, pin_memory=True)
@@ -757,8 +768,14 @@ def main():
                          "lstm_fast": (8.768533e9 + 0.394084e9) / 12.5e6}
     row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
-        bytes_per_launch = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
+        # SURVEY 8(d)'s per-unit figure: decision records read (32 B per
+        # scheduled stage) + the state's feature matrix written (128 B per
+        # row, all T rows); the kernel physically moves far less (16 B
+        # records or 2 B codes, 32 B acquired rows for scheduled stages only:
+        # `physical`), which is why it is issue-bound rather than HBM-bound
+        bytes_per_launch = n_records * 32 + M * T * ROW_BYTES
         achieved = bytes_per_launch / (avg[dom] / 1e3) / 1e9
+        phys = n_records * (RECORD_BYTES + row_bytes) + 8 * (M + 1)
         peak = peaks.get("hbm_gbs", 6650.0)
         tr = traffic_per_state.get(dom)
         roof = {"kernel": "k_featurize_rows", "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -766,7 +783,9 @@ def main():
                 "traffic": tr * M if tr and mode == _lib.MODE_FAST else None,
                 "traffic_source": TRAFFIC_SOURCE,
                 "bytes_per_launch": bytes_per_launch,
-                "algorithmic": f"16 B record read + {row_bytes} B row written per scheduled stage"}
+                "algorithmic": "SURVEY 8(d): 32 B per scheduled stage (records) + 128 B x T (feature rows)",
+                "physical": {"bytes_per_launch": phys, "achieved_gbs": phys / (avg[dom] / 1e3) / 1e9,
+                             "what": f"16 B record read + {row_bytes} B row written per scheduled stage"}}
     else:
         flops_per_launch = FLOPS_PER_STEP * timesteps
         achieved = flops_per_launch / (avg[dom] / 1e3) / 1e12

@@ -2216,7 +2216,14 @@ static int launch_grads(ts_ctx* ctx, tr::TrainArgs& a, int mode, double* grad, d
   if (mode == TS_TRAIN_TCF) {
     // forward and backward recurrences on the tensor cores (ts_train_tc.cuh)
     if (H != trc::H) return fail(ctx, TS_ERR_ARG, "tensor-core training needs hidden size 32");
-    const int n_tiles = (int)((B + trc::TM - 1) / trc::TM);
+    // sequences per tile: 128 when the batch fills the SMs, else fewer (a
+    // multiple of 32, every tile's recurrence is latency-bound, so more
+    // partly filled tiles finish sooner than fewer full ones)
+    int rows = trc::TM;
+    if (B < (int64_t)trc::TM * ctx->sm_count)
+      rows = std::max<int>(32, (int)(((B + ctx->sm_count - 1) / ctx->sm_count + 31) / 32 * 32));
+    if (const char* e = getenv("TS_TRC_ROWS")) rows = std::min(trc::TM, std::max(1, atoi(e)));
+    const int n_tiles = (int)((B + rows - 1) / rows);
     const size_t img_bytes = tc::TILE_BYTES + 128 + 2 * trc::WT_BYTES;
     TS_CUDA(ctx->trc_img.reserve(img_bytes, ctx->stream));
     TS_CUDA(ctx->tr_cache.reserve(sizeof(float) * (size_t)n_tiles * Tmax * trc::NF * 4 * trc::TM * 8, ctx->stream));
@@ -2240,6 +2247,7 @@ static int launch_grads(ts_ctx* ctx, tr::TrainArgs& a, int mode, double* grad, d
     ta.n_total = a.n_total;
     ta.draw_in = a.draw_in;
     ta.partial = ctx->tr_partial.as<double>();
+    ta.rows = rows;
     ta.dmax = reinterpret_cast<unsigned*>(ctx->tr_partial.as<double>() + (size_t)n_tiles * L.n);
     TS_CUDA(cudaMemsetAsync(ta.dmax, 0, sizeof(unsigned), ctx->stream));
     trc::k_trc_pack<<<32, 256, 0, ctx->stream>>>(a.P, ctx->trc_img.as<uint8_t>());

@@ -79,6 +79,8 @@ struct Args {
   const double* draw_in;   // optional caller d_raw (lstm_backward)
   unsigned* dmax;          // max |d_raw| as float bits (zeroed before k_trc_fwd)
   double* partial;         // [n_tiles][n_params]
+  int rows;                // sequences per tile (<= 128; the rest of the tile's TMEM lanes idle):
+                           // small batches spread over more SMs - the recurrences are latency-bound
 };
 
 __device__ __forceinline__ size_t cache_at(int tile, int t, int Tmax, int fld, int g8, int r) {
@@ -202,9 +204,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_trc_fwd(Args a) {
     tc::mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int b = tile * TM + r;
+  const int b = tile * a.rows + r;
   int idx = 0, T = 0, d = 0;
-  if (b < a.B) {
+  if (r < a.rows && b < a.B) {
     idx = a.batch[b];
     T = a.D.Tlen[idx];
     d = a.D.depth[idx];
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_trc_fwd(Args a) {
   __syncthreads();
   if (wg == 0) {
     double dr = 0.0;
-    if (b < a.B) {
+    if (r < a.rows && b < a.B) {
       double rw = fmul((double)T, a.P[L.obout]);
       for (int q = 0; q < NWG; ++q) rw = fadd(rw, rawp[q * TM + r]);
       dr = a.draw_in ? a.draw_in[b] : fdiv(fmul(2.0, fsub(fadd(rw, a.target_scale), a.D.logt[idx])), a.n_total);
@@ -388,10 +390,10 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_trc_bwd(Args a) {
     tc::mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int b = tile * TM + r;
+  const int b = tile * a.rows + r;
   int idx = 0, T = 0, d = 0;
   double dr = 0.0;
-  if (b < a.B) {
+  if (r < a.rows && b < a.B) {
     idx = a.batch[b];
     T = a.D.Tlen[idx];
     d = a.D.depth[idx];

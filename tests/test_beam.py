@@ -1,7 +1,8 @@
 """beam_search (search.py:115-133) against the unmodified reference's
 results (tests/golden/beam.json, tools/make_golden_beam.py): width 1/3/8
 from the initial state and width 8 (4 on ResNet-18) from mid-schedule
-prefixes, on the toys, p12_deep, crp2d, VGG-16 and ResNet-18.  The oracle's
+prefixes, on the toys, p12_deep, crp2d, VGG-16, ResNet-18, MobileNet-v2 and
+ResNet-50 (the paper's DNN benchmarks, width 8).  The oracle's
 beam is checked against the same fixtures on the small pipelines (CPU);
 the fused device beam (ts_beam) and the generic loop over the device
 V-callable must both return the reference's schedule."""
@@ -61,7 +62,7 @@ def test_generic_beam_over_device_v_matches_reference(v0_path):
     V = model_value(params)
     plain = lambda states: V(states)  # noqa: E731  (no .beam attribute)
     for key, c in _cases().items():
-        if "resnet18" in key:
+        if "resnet" in key or "mobilenet" in key:
             continue  # the generic loop materializes every child on the host
         p = pi.parse_pipeline(c["text"])
         s = beam_search(_prefix_state(p, c["prefix"]), plain, c["width"])

@@ -29,8 +29,13 @@ def case_list():
             out.append((f, w, 0))
         out.append((f, 8, 2))  # from a 2-decision prefix
     out += [("assets/pipelines/nets/vgg16.pl", 8, 0), ("assets/pipelines/nets/vgg16.pl", 8, 17),
-            ("assets/pipelines/nets/resnet18.pl", 8, 0), ("assets/pipelines/nets/resnet18.pl", 4, 30)]
+            ("assets/pipelines/nets/resnet18.pl", 8, 0), ("assets/pipelines/nets/resnet18.pl", 4, 30),
+            ("assets/pipelines/nets/mobilenet_v2.pl", 8, 0), ("assets/pipelines/nets/resnet50.pl", 8, 0)]
     return out
+
+
+def key_of(f, width, plen):
+    return f"{f}|w{width}|p{plen}"
 
 
 def path_of(f):
@@ -62,11 +67,19 @@ def run(case):
 
 
 def main():
+    """--missing: only the cases not yet in beam.json (the slow ones can be
+    added without recomputing the rest)."""
+    path = ROOT / "tests" / "golden" / "beam.json"
     cases = case_list()
-    with mp.get_context("spawn").Pool(min(8, len(cases))) as pool:
+    old = {}
+    if "--missing" in sys.argv and path.exists():
+        old = json.loads(path.read_text())
+        cases = [c for c in cases if key_of(*c) not in old]
+    with mp.get_context("spawn").Pool(max(1, min(8, len(cases)))) as pool:
         res = pool.map(run, cases)
-    out = {f"{r['file']}|w{r['width']}|p{len(r['prefix'])}": r for r in res}
-    (ROOT / "tests" / "golden" / "beam.json").write_text(json.dumps(out, indent=0) + "\n")
+    out = dict(old)
+    out.update({key_of(r["file"], r["width"], len(r["prefix"])): r for r in res})
+    path.write_text(json.dumps(out, indent=0) + "\n")
     for k, r in out.items():
         print(k, round(r["reference_wall_s"], 2), "s")
 
