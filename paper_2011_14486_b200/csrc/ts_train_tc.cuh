@@ -262,16 +262,34 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_trc_fwd(Args a) {
     float gi[8], gf[8], gg[8], go[8], h8[8];
     float acc = 0.0f;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      gi[u] = sigm_s(ui[u]);
-      gf[u] = sigm_s(uf[u]);
-      gg[u] = tanh_s(vg[u]);
-      go[u] = sigm_s(uo[u]);
-      const float cn = fmaf(gf[u], c[u], gi[u] * gg[u]);
-      c[u] = act ? cn : c[u];
-      h8[u] = go[u] * tanh_s(C2 * c[u]);
-      acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
-      hs[u] += act ? h8[u] : 0.0f;
+    for (int u = 0; u < 8; u += 2) {
+      // gates with shared reciprocals (Montgomery batch inversion: 1/a =
+      // b/(ab)): (i, f) and (g, o) per unit, tanh(c) per pair of units -
+      // 5 ex2 + 2.5 rcp per unit instead of 5 + 5; exponents clamped at 40
+      // so the products stay finite (sigma >= 2^-40)
+      float tcn[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int v = u + q;
+        const float ti = 1.0f + tc::ex2(fminf(ui[v], 40.0f)), tf = 1.0f + tc::ex2(fminf(uf[v], 40.0f));
+        const float tg = 1.0f + tc::ex2(fminf(vg[v], 40.0f)), to = 1.0f + tc::ex2(fminf(uo[v], 40.0f));
+        const float r1 = tc::rcp(ti * tf), r2 = tc::rcp(tg * to);
+        gi[v] = tf * r1;
+        gf[v] = ti * r1;
+        gg[v] = fmaf(2.0f, to * r2, -1.0f);
+        go[v] = tg * r2;
+        const float cn = fmaf(gf[v], c[v], gi[v] * gg[v]);
+        c[v] = act ? cn : c[v];
+        tcn[q] = 1.0f + tc::ex2(fminf(C2 * c[v], 40.0f));
+      }
+      const float r3 = tc::rcp(tcn[0] * tcn[1]);
+      h8[u] = go[u] * fmaf(2.0f, tcn[1] * r3, -1.0f);
+      h8[u + 1] = go[u + 1] * fmaf(2.0f, tcn[0] * r3, -1.0f);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        acc = fmaf(h8[u + q], wout[g8 * 8 + u + q], acc);
+        hs[u + q] += act ? h8[u + q] : 0.0f;
+      }
     }
     if (act) {
       float* cc = a.cache + cache_at(tile, t, a.Tmax, 0, g8, r);
