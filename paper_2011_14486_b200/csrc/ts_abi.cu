@@ -1839,7 +1839,7 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
   }
   // device state rows of the frontier, double-buffered: [width][T][F]
   const size_t frow = (size_t)T * F;
-  TS_CUDA(ctx->beam_rows.reserve(sizeof(double) * frow * 2 * width));
+  TS_CUDA(ctx->beam_rows.reserve(sizeof(double) * frow * 2 * width, ctx->stream));
   TS_CUDA(ctx->h_sel.reserve(sizeof(int) * 2 * width));
   double* cur = ctx->beam_rows.as<double>();
   double* nxt = cur + frow * width;
@@ -2372,6 +2372,7 @@ int ts_lstm_backward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t
   }
   // the batch as a training dataset: sequence i = init rows i*T .. i*T+T-1
   // (no scheduled rows), batch = 0..B-1, d_raw given
+  if (B * T > INT32_MAX) return fail(ctx, TS_ERR_ARG, "batch x sequence too large");
   std::vector<int32_t> meta(3 * B + B);
   std::vector<int64_t> rb(B, 0);
   for (int64_t i = 0; i < B; ++i) {
@@ -2380,7 +2381,6 @@ int ts_lstm_backward(ts_ctx* ctx, const double* X, int64_t B, int64_t T, int64_t
     meta[2 * B + i] = 0;             // depth
     meta[3 * B + i] = (int32_t)i;    // batch
   }
-  if (B * T > INT32_MAX) return fail(ctx, TS_ERR_ARG, "batch x sequence too large");
   TS_CUDA(ctx->bk_X.reserve(sizeof(double) * B * T * F, ctx->stream));
   TS_CUDA(ctx->bk_meta.reserve(sizeof(int32_t) * 4 * B + sizeof(int64_t) * B, ctx->stream));
   TS_CUDA(ctx->bk_P.reserve(sizeof(double) * (L.n + L.n + 2 * B), ctx->stream));
