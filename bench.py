@@ -237,6 +237,14 @@ def _ref_cost_worker(args):
     return n / (time.perf_counter() - t0)
 
 
+def net_path(net):
+    """Benchmark networks (assets/pipelines/nets) and the reference's own
+    3-layer chain t3_chain (configs[0]: its copy in oracle/_ref/assets)."""
+    if net == "t3_chain":
+        return ROOT / "oracle" / "_ref" / "assets" / "pipelines" / "toys" / "t3_chain.pl"
+    return ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl"
+
+
 def _ref_search_worker(task):
     """The reference's own search with its model_value V-callable
     (cli.py:cmd_schedule's timed region, cli.py:226-232) on one benchmark
@@ -249,7 +257,7 @@ def _ref_search_worker(task):
     from tensched.search import beam_search, greedy_schedule, model_value
     from tensched.value_model import load
     params = load(str(GOLD / "v0.ckpt"))
-    p = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
+    p = parse_pipeline(net_path(net).read_text())
     V = model_value(params)
     t0 = time.perf_counter()
     if kind == "beam":
@@ -266,6 +274,36 @@ def reference_search(tasks):
     import multiprocessing as mp
     with mp.get_context("spawn").Pool(len(tasks)) as pool:
         return {r[0]: r[1:] for r in pool.map(_ref_search_worker, tasks)}
+
+
+def reference_gradients_rate(n=512, reps=3):
+    """The reference's value_model.gradients (value_model.py:182-210, numpy
+    BPTT) on n VGG-16 (partial schedule, target) pairs with their features
+    cached ('samples/s, features cached'), this host,
+    numpy's default BLAS threads."""
+    _ref_import()
+    from tensched.featurizer import featurize_state
+    from tensched.pipeline_ir import parse_pipeline
+    from tensched.schedule_space import apply, candidate_actions, initial_state
+    from tensched.search import SearchRng
+    from tensched.value_model import gradients, load
+    params = load(str(GOLD / "v0.ckpt"))
+    p = parse_pipeline(VGG.read_text())
+    batch = []
+    for seed in range(30_000_000, 30_000_000 + n):
+        rng = SearchRng(seed)
+        d = rng.randrange(len(p.stages)) + 1
+        s = initial_state(p)
+        for _ in range(d):
+            c = candidate_actions(s)
+            s = apply(s, c[rng.randrange(len(c))])
+        featurize_state(s)  # cached on the state: timing covers the gradient only
+        batch.append((s, 1000.0 + seed % 977))
+    gradients(params, batch)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        gradients(params, batch)
+    return n * reps / (time.perf_counter() - t0)
 
 
 def run_reference_arm(args):
@@ -862,8 +900,10 @@ def main():
     greedy, beam, level1 = {}, {}, None
     if rank == 0 and not args.no_greedy:
         from paper_2011_14486_b200.search import greedy_schedule_gpu
-        for net in ("crp2d", "resnet18", "resnet50", "mobilenet_v2"):
-            pn = parse_pipeline((ROOT / "assets" / "pipelines" / "nets" / f"{net}.pl").read_text())
+        for net in ("t3_chain", "crp2d", "vgg16", "resnet18", "resnet50", "mobilenet_v2"):
+            if not net_path(net).exists():
+                continue
+            pn = parse_pipeline(net_path(net).read_text())
             t0 = time.perf_counter()
             greedy_schedule_gpu(pn, params)  # first call: descriptor upload, init rows, prefix states
             first = time.perf_counter() - t0
@@ -930,6 +970,13 @@ def main():
                 train_line["cost_oracle"]["cpu_reference_1proc"] = _ref_cost_worker((5_000_000, 100))
             except Exception as e:
                 train_line["cost_oracle"]["cpu_reference_1proc"] = f"unavailable: {e}"
+            try:  # the reference's own gradients (numpy BPTT), features cached
+                train_line["cpu_reference"] = {
+                    "value": reference_gradients_rate(), "unit": "samples/s",
+                    "what": "tensched.value_model.gradients on 512 VGG-16 pairs (T=34), features cached, "
+                            "numpy default BLAS threads, this host"}
+            except Exception as e:
+                train_line["cpu_reference"] = f"unavailable: {e}"
 
     if rank == 0:
         line = {
