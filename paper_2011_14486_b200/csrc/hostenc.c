@@ -7,10 +7,12 @@
  * records (state._cache["ts_records"], featurizer.py:72-73's cache idiom)
  * is copied; otherwise every decision object is looked up by identity in an
  * open-addressing table (pointer -> schedule index + record; the table holds
- * a reference, so the pointer stays valid) and only unseen objects call back
- * into Python (_PipelineInfo.encode: validation + encoding, cached by value
- * there).  Search children share all but their last decision object with
- * their parent, so a child costs one identity probe per decision.
+ * a reference, so the pointer stays valid); an unseen object is looked up by
+ * value ((index, its seven fields) -> record, a dict held here: the same
+ * action built again by candidate_actions), and only unseen values call back
+ * into Python (_PipelineInfo.encode: validation + encoding).  Search
+ * children share all but their last decision object with their parent, so a
+ * child costs one identity probe per decision and one value lookup.
  *
  * Module _hostenc (CPython C API, built in-tree by build.py):
  *   encode_group(states, idxs, T, fallback) -> (records: bytes, offsets: bytes [int64 n+1])
@@ -27,13 +29,19 @@ typedef struct {
   uint8_t rec[16];
 } Slot;
 
-#define CAP_LOG2 20
+#define CAP_LOG2 18
 #define CAP (1u << CAP_LOG2)
 static Slot* table = NULL;
 static size_t used = 0;
 static PyObject* s_cache = NULL;   /* "_cache" */
 static PyObject* s_records = NULL; /* "ts_records" */
 static PyObject* s_decisions = NULL;
+/* decision fields: the value key of a decision object (its dataclass fields,
+ * search.py / schedule_space.py LayerSchedule) */
+static PyObject* s_fields[7] = {NULL};
+static const char* field_names[7] = {"stage", "splits", "order", "vectorize_width", "parallel", "compute_at",
+                                     "store_at"};
+static PyObject* content = NULL; /* (j, fields...) -> 16-byte record (bytes) */
 
 static void table_clear(void) {
   if (!table) return;
@@ -68,8 +76,45 @@ static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
   }
   PyObject* jj = PyLong_FromLong(j); /* a cached small int */
   if (!jj) return -1;
-  PyObject* argv[2] = {jj, d};
-  PyObject* r = PyObject_Vectorcall(fallback, argv, 2, NULL);
+  /* a new object: look its value up (a decision equal to one already
+   * encoded at this index - candidate_actions builds new objects for the
+   * same actions), else the Python encoder validates and encodes it */
+  PyObject* key = PyTuple_New(8);
+  if (!key) {
+    Py_DECREF(jj);
+    return -1;
+  }
+  Py_INCREF(jj);
+  PyTuple_SET_ITEM(key, 0, jj);
+  int have_key = 1;
+  for (int f = 0; f < 7; ++f) {
+    PyObject* v = PyObject_GetAttr(d, s_fields[f]);
+    if (!v) { /* not decision-like: the fallback reports it */
+      PyErr_Clear();
+      have_key = 0;
+      break;
+    }
+    PyTuple_SET_ITEM(key, 1 + f, v);
+  }
+  PyObject* r = NULL;
+  if (have_key) {
+    r = PyDict_GetItemWithError(content, key); /* borrowed */
+    if (r) {
+      Py_INCREF(r);
+    } else if (PyErr_Occurred()) { /* unhashable fields: the fallback decides */
+      PyErr_Clear();
+      have_key = 0;
+    }
+  }
+  if (!r) {
+    PyObject* argv[2] = {jj, d};
+    r = PyObject_Vectorcall(fallback, argv, 2, NULL);
+    if (r && have_key && PyBytes_Check(r)) {
+      if (PyDict_GET_SIZE(content) >= (1 << 20)) PyDict_Clear(content);
+      if (PyDict_SetItem(content, key, r) < 0) PyErr_Clear();
+    }
+  }
+  Py_DECREF(key);
   Py_DECREF(jj);
   if (!r) return -1;
   if (!PyBytes_Check(r) || PyBytes_GET_SIZE(r) != 16) {
@@ -237,6 +282,7 @@ static PyObject* clear(PyObject* self, PyObject* args) {
   (void)self;
   (void)args;
   table_clear();
+  PyDict_Clear(content);
   Py_RETURN_NONE;
 }
 
@@ -252,5 +298,8 @@ PyMODINIT_FUNC PyInit__hostenc(void) {
   s_records = PyUnicode_InternFromString("ts_records");
   s_decisions = PyUnicode_InternFromString("decisions");
   if (!s_cache || !s_records || !s_decisions) return NULL;
+  for (int f = 0; f < 7; ++f)
+    if (!(s_fields[f] = PyUnicode_InternFromString(field_names[f]))) return NULL;
+  if (!(content = PyDict_New())) return NULL;
   return PyModule_Create(&module);
 }
