@@ -1,3 +1,6 @@
+"""Where the INTEGRATION level-1 V call spends its time on the reference's
+own ScheduleState children of a VGG-16 walk: host encoding (cold) vs the
+device call with records cached (first and repeat)."""
 import sys, time
 sys.path.insert(0, "."); sys.argv = ["x"]
 import bench
@@ -22,6 +25,3 @@ t0 = time.perf_counter(); ss.encode_states(k); t1 = time.perf_counter()
 v = V(k); t2 = time.perf_counter()
 v = V(k); t3 = time.perf_counter()
 print(f"{len(k)} kids: encode {1e3*(t1-t0):.2f} ms, V (records cached) {1e3*(t2-t1):.2f} ms, V again {1e3*(t3-t2):.2f} ms")
-import cProfile, pstats
-cProfile.run("V(k)", "/tmp/l1.prof")
-pstats.Stats("/tmp/l1.prof").sort_stats("cumtime").print_stats(12)

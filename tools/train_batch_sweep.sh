@@ -1,3 +1,4 @@
+# V-training throughput per gradient mode at two per-GPU batch sizes (bench.py v_training).
 for B in 4096 16384; do
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-greedy --big-states 0 --no-exact --train-batch $B > gpurun_out/bt_$B.log 2>&1
 python - $B <<'PY'
