@@ -16,6 +16,13 @@ sys.path.insert(0, str(ROOT / "oracle"))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU oracle checks")
+    # a fresh checkout has no built artefacts (they are git-ignored): build
+    # the in-tree library and host encoder before anything imports them
+    from paper_2011_14486_b200 import build as _build
+    try:
+        _build.build()
+    except Exception as e:  # e.g. no nvcc on this host: the tests that need it report it
+        sys.stderr.write(f"conftest: native build skipped ({e})\n")
 
 
 @pytest.fixture(scope="session")
