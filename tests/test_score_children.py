@@ -48,7 +48,7 @@ def test_children_values_bit_identical(greedy_golden, v0, v0_path):
             want = predict_states(v0, kids)
             assert np.array_equal(bits(got), bits(want)), (key, len(s.decisions))
             oracle_v = O.values(oparams, P, [[O.as_act(d) for d in k.decisions] for k in kids[:8]])
-            np.testing.assert_allclose(got[:8], oracle_v, rtol=1e-12, atol=0)
+            assert np.array_equal(bits(got[:8]), bits(oracle_v))
 
 
 def test_children_argmin_with_noise(greedy_golden, v0):
