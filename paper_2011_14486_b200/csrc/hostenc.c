@@ -8,14 +8,18 @@
  * is copied; otherwise every decision object is looked up by identity in an
  * open-addressing table (pointer -> schedule index + record; the table holds
  * a reference, so the pointer stays valid); an unseen object is looked up by
- * value ((index, its seven fields) -> record, a dict held here: the same
- * action built again by candidate_actions), and only unseen values call back
- * into Python (_PipelineInfo.encode: validation + encoding).  Search
+ * value ((index, its seven fields) -> record: the same action built again by
+ * candidate_actions) in the pipeline's own value dict (_PipelineInfo.val_cache,
+ * filled by the Python encoder), and only unseen values call back into Python
+ * (_PipelineInfo.encode: validation + encoding).  Both caches are per
+ * pipeline: a record depends on the stage's loop table and its sole consumer,
+ * so the same (index, fields) can encode differently - or be illegal - in
+ * another pipeline.  Identity slots carry their owner (the value dict).  Search
  * children share all but their last decision object with their parent, so a
  * child costs one identity probe per decision and one value lookup.
  *
  * Module _hostenc (CPython C API, built in-tree by build.py):
- *   encode_group(states, idxs, T, fallback) -> (records: bytes, offsets: bytes [int64 n+1])
+ *   encode_group(states, idxs, T, fallback, vcache) -> (records: bytes, offsets: bytes [int64 n+1])
  *   clear() -> None   (drop the identity table)
  */
 #define PY_SSIZE_T_CLEAN
@@ -24,7 +28,8 @@
 #include <string.h>
 
 typedef struct {
-  PyObject* obj; /* strong reference; NULL = empty slot */
+  PyObject* obj;   /* strong reference; NULL = empty slot */
+  PyObject* owner; /* strong reference: the pipeline's value dict */
   int32_t idx;
   uint8_t rec[16];
 } Slot;
@@ -41,34 +46,36 @@ static PyObject* s_decisions = NULL;
 static PyObject* s_fields[7] = {NULL};
 static const char* field_names[7] = {"stage", "splits", "order", "vectorize_width", "parallel", "compute_at",
                                      "store_at"};
-static PyObject* content = NULL; /* (j, fields...) -> 16-byte record (bytes) */
 
 static void table_clear(void) {
   if (!table) return;
   for (size_t i = 0; i < CAP; ++i) {
     if (table[i].obj) {
       Py_DECREF(table[i].obj);
+      Py_DECREF(table[i].owner);
       table[i].obj = NULL;
+      table[i].owner = NULL;
     }
   }
   used = 0;
 }
 
-static inline size_t slot_of(const void* p) {
-  uint64_t h = (uint64_t)(uintptr_t)p;
+static inline size_t slot_of(const void* p, const void* owner) {
+  uint64_t h = (uint64_t)(uintptr_t)p ^ ((uint64_t)(uintptr_t)owner << 7);
   h ^= h >> 33;
   h *= 0xff51afd7ed558ccdull;
   h ^= h >> 33;
   return (size_t)(h & (CAP - 1));
 }
 
-/* record of decision d at schedule index j: table hit or Python fallback */
-static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
-  size_t s = slot_of(d);
+/* record of decision d at schedule index j of the pipeline whose value dict
+ * is vcache: table hit, value hit or Python fallback */
+static int record_of(PyObject* d, int j, PyObject* fallback, PyObject* vcache, uint8_t* out) {
+  size_t s = slot_of(d, vcache);
   for (;;) {
     Slot* e = &table[s];
     if (!e->obj) break;
-    if (e->obj == d && e->idx == j) {
+    if (e->obj == d && e->idx == j && e->owner == vcache) {
       memcpy(out, e->rec, 16);
       return 0;
     }
@@ -98,7 +105,7 @@ static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
   }
   PyObject* r = NULL;
   if (have_key) {
-    r = PyDict_GetItemWithError(content, key); /* borrowed */
+    r = PyDict_GetItemWithError(vcache, key); /* borrowed */
     if (r) {
       Py_INCREF(r);
     } else if (PyErr_Occurred()) { /* unhashable fields: the fallback decides */
@@ -107,12 +114,8 @@ static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
     }
   }
   if (!r) {
-    PyObject* argv[2] = {jj, d};
+    PyObject* argv[2] = {jj, d}; /* fills vcache itself */
     r = PyObject_Vectorcall(fallback, argv, 2, NULL);
-    if (r && have_key && PyBytes_Check(r)) {
-      if (PyDict_GET_SIZE(content) >= (1 << 20)) PyDict_Clear(content);
-      if (PyDict_SetItem(content, key, r) < 0) PyErr_Clear();
-    }
   }
   Py_DECREF(key);
   Py_DECREF(jj);
@@ -125,10 +128,12 @@ static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
   memcpy(out, PyBytes_AS_STRING(r), 16);
   Py_DECREF(r);
   if (used >= CAP / 2) table_clear(); /* bounded: foreign callers bring new objects */
-  s = slot_of(d);
+  s = slot_of(d, vcache);
   while (table[s].obj) s = (s + 1) & (CAP - 1);
   Py_INCREF(d);
+  Py_INCREF(vcache);
   table[s].obj = d;
+  table[s].owner = vcache;
   table[s].idx = j;
   memcpy(table[s].rec, out, 16);
   ++used;
@@ -137,9 +142,9 @@ static int record_of(PyObject* d, int j, PyObject* fallback, uint8_t* out) {
 
 static PyObject* encode_group(PyObject* self, PyObject* args) {
   (void)self;
-  PyObject *states, *idxs, *fallback;
+  PyObject *states, *idxs, *fallback, *vcache;
   Py_ssize_t T;
-  if (!PyArg_ParseTuple(args, "OOnO", &states, &idxs, &T, &fallback)) return NULL;
+  if (!PyArg_ParseTuple(args, "OOnOO!", &states, &idxs, &T, &fallback, &PyDict_Type, &vcache)) return NULL;
   if (!table) {
     table = (Slot*)PyMem_Calloc(CAP, sizeof(Slot));
     if (!table) return PyErr_NoMemory();
@@ -237,7 +242,7 @@ static PyObject* encode_group(PyObject* self, PyObject* args) {
     }
     PyObject* const* dv = PySequence_Fast_ITEMS(dq);
     for (Py_ssize_t j = 0; j < m; ++j) {
-      if (record_of(dv[j], (int)j, fallback, buf + (len + j) * 16)) {
+      if (record_of(dv[j], (int)j, fallback, vcache, buf + (len + j) * 16)) {
         Py_DECREF(dq);
         Py_XDECREF(cache);
         goto fail;
@@ -282,7 +287,6 @@ static PyObject* clear(PyObject* self, PyObject* args) {
   (void)self;
   (void)args;
   table_clear();
-  PyDict_Clear(content);
   Py_RETURN_NONE;
 }
 
@@ -300,6 +304,5 @@ PyMODINIT_FUNC PyInit__hostenc(void) {
   if (!s_cache || !s_records || !s_decisions) return NULL;
   for (int f = 0; f < 7; ++f)
     if (!(s_fields[f] = PyUnicode_InternFromString(field_names[f]))) return NULL;
-  if (!(content = PyDict_New())) return NULL;
   return PyModule_Create(&module);
 }

@@ -286,7 +286,7 @@ def encode_states(states):
         inf = _info(p)
         if _hostenc is not None:  # native: one C call per group (csrc/hostenc.c)
             try:
-                rb, ob = _hostenc.encode_group(states, idxs, inf.T, inf.encode)
+                rb, ob = _hostenc.encode_group(states, idxs, inf.T, inf.encode, inf.val_cache)
             except ValueError as e:
                 raise IllegalActionError(str(e)) from None
             recs = np.frombuffer(rb, dtype=_lib.DECISION_DTYPE)

@@ -293,3 +293,30 @@ def test_native_host_encoder_matches_python_path(greedy_golden):
     bad = ss.ScheduleState(p, tuple(ss.initial_state(p).decisions) + (ss.LayerSchedule("nope", (), ("x",)),))
     with pytest.raises(IllegalActionError):
         ss.encode_states([bad])
+
+
+def test_native_host_encoder_caches_are_per_pipeline(greedy_golden):
+    """A record depends on the pipeline (the stage's loop table, its sole
+    consumer), so the native encoder's identity and value caches must not
+    carry a decision across pipelines: t3_chain's conv decision
+    compute_at=(relu, 0) is legal there and illegal in a variant where pool
+    also reads conv - reusing the same decision objects, or equal ones, must
+    still raise in the variant (schedule_space.py:299-305 sole-consumer
+    rule)."""
+    import dataclasses
+
+    assert ss._hostenc is not None, "the native host encoder is not built"
+    text = greedy_golden["ref:pipelines/toys/t3_chain.pl"]["text"]
+    a = pi.parse_pipeline(text)
+    b = pi.parse_pipeline(text.replace("in relu map x*2+2", "in relu map x*2+2\n  in conv map x*2+1"))
+    s = ss.initial_state(a)
+    for _ in range(3):
+        s = ss.apply(s, ss.candidate_actions(s)[-1])
+    assert s.decisions[2].compute_at == ("relu", 0)
+    copies = tuple(dataclasses.replace(d) for d in s.decisions)
+    for decs in (s.decisions, copies):  # fresh states: no cached records, the tables fill
+        recs = ss.encode_states([ss.ScheduleState(a, decs)])[0][2]
+        assert list(recs["anchor"]) == [-1, 1, 0]
+    for decs in (s.decisions, copies):
+        with pytest.raises(IllegalActionError, match="sole consumer"):
+            ss.encode_states([ss.ScheduleState(b, decs)])
