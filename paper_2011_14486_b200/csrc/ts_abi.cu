@@ -155,6 +155,7 @@ struct ts_ctx {
   DevBuf resc, resc2;  // k_rescore_exact scratch rows, per lane
   DevBuf bk_X, bk_meta, bk_P;  // ts_lstm_backward: the batch, its layout, params + gradient
   DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
+  DevBuf ghash;                 // ts_greedy: per-layer children row hashes [T][4096] + counts [T]
   DevBuf trc_img;               // TS_TRAIN_TCF: per-step packed weight images
   bool trc_attr_set = false;
   DevBuf beam_rows;             // ts_beam: frontier state rows, double-buffered
@@ -1456,6 +1457,21 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   TS_CUDA(cudaMemsetAsync(ctx->gstat.p, 0, sizeof(unsigned long long), ctx->stream));
   const PipelineDesc& D = *P->h;
   const int T = D.n_stages;
+  constexpr int kMaxChildren = 4096;
+  // fused layers (H = 32): children row hashes per layer for the distinct
+  // count, and the layer ticket, zeroed once (each layer's last block re-zeroes it)
+  const bool fused_layers = ctx->hidden == 32;
+  unsigned long long* ghash = nullptr;
+  int* gcount = nullptr;
+  int* gticket = nullptr;
+  if (fused_layers) {
+    const size_t hb = sizeof(unsigned long long) * (size_t)T * kMaxChildren;
+    TS_CUDA(ctx->ghash.reserve(hb + sizeof(int) * (size_t)(T + 1), ctx->stream));
+    ghash = ctx->ghash.as<unsigned long long>();
+    gcount = reinterpret_cast<int*>(ctx->ghash.as<char>() + hb);
+    gticket = gcount + T;
+    TS_CUDA(cudaMemsetAsync(gcount, 0, sizeof(int) * (size_t)(T + 1), ctx->stream));
+  }
   std::vector<Nest> nests(T);
   std::vector<ts_decision> cands;
   cands.reserve(1024);
@@ -1489,13 +1505,13 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     if (trace) t_enum += now_us() - te0;
     if (cnt <= 0) return fail(ctx, cnt < 0 ? (int)-cnt : TS_ERR_PIPELINE, "candidate enumeration");
     const int n = (int)cnt;
-    if (n > 4096) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
+    if (n > kMaxChildren) return fail(ctx, TS_ERR_PIPELINE, "more than 4096 candidates in one layer");
     TS_CUDA(ctx->records.reserve(sizeof(ts_decision) * (n + 8)));
     TS_CUDA(ctx->rows.reserve(sizeof(double) * F * n));
     TS_CUDA(ctx->reps.reserve(sizeof(int) * (n + 1)));
     TS_CUDA(ctx->raw.reserve(sizeof(double) * n));
     TS_CUDA(ctx->out.reserve(sizeof(double) * 3));
-    const bool fused = ctx->hidden == 32;  // H = 32: the 2-kernel layer with the last-block argmin
+    const bool fused = fused_layers;  // H = 32: the one-kernel layer with the last-block argmin
     // stage host data in pinned memory: candidate records, then the consumer
     // nest right behind them (one H2D per layer)
     ts_decision* hs = ctx->h_stage.as<ts_decision>();
@@ -1503,27 +1519,27 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     Nest* hn = reinterpret_cast<Nest*>(hs + n);
     static_assert(sizeof(Nest) <= 8 * sizeof(ts_decision), "nest staging");
     if (cn) *hn = *cn;
-    int* ticket = ctx->reps.as<int>() + n;
     if (fused) {
-      // H = 32: the kernels read the candidates and the consumer nest from
-      // the mapped staging buffer (no copy), the exact kernel is a
-      // programmatic dependent of the rows kernel (its weight loads overlap
-      // it), and the last block writes the layer's result into mapped host
-      // memory, which the host polls (no copy, no stream sync)
-      if (!ctx->exact_attr_set) {
-        TS_CUDA(cudaFuncSetAttribute(k_score_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(ExactSmem)));
-        TS_CUDA(cudaFuncSetAttribute(k_children_exact32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(ExactSmem)));
-        ctx->exact_attr_set = true;
-      }
-      k_children_rows_dedup<<<1, 1024, 0, ctx->stream>>>(
-          P->d.as<PipelineDesc>(), s, hs, n, cn ? hn : nullptr, P->init_raw.as<double>(),
-          ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->reps.as<int>(),
-          ctx->status.as<int>(), ticket, ctx->gstat.as<unsigned long long>());
-      TS_LAUNCHED();
+      // H = 32: ONE kernel per layer - every block computes its child's row
+      // from the candidate and the consumer nest in the mapped staging buffer
+      // (no copy), runs the exact LSTM over the T - s timesteps it differs
+      // in, and the last block to finish runs the argmin, installs the
+      // winner's row and writes the layer's result into mapped host memory,
+      // which the host polls (no copy, no stream sync)
+      ChildRow cr;
+      cr.P = P->d.as<PipelineDesc>();
+      cr.cands = hs;
+      cr.cnest = cn ? hn : nullptr;
+      cr.init_raw = P->init_raw.as<double>();
+      cr.mean = ctx->mean.as<double>();
+      cr.stdv = ctx->stdv.as<double>();
+      cr.rows_out = ctx->rows.as<double>();
+      cr.hashes = ghash + (size_t)i * kMaxChildren;
+      cr.counts = gcount + i;
+      cr.status = ctx->status.as<int>();
       GreedyTail tail;
-      tail.ticket = ticket;
+      tail.ticket = gticket;
+      tail.reset_ticket = 1;
       tail.out = ctx->out.as<double>();
       volatile double* ho = ctx->h_out.as<double>();
       const double seq = (double)++ctx->greedy_seq;
@@ -1540,23 +1556,9 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       if (xs_bytes > 40 * 1024)  // with the kernel's static shared memory
         TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)xs_bytes));
-      {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)n);
-        cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = xs_bytes;
-        cfg.stream = ctx->stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        TS_CUDA(cudaLaunchKernelEx(&cfg, k_children_exact_mw, lstm_weights(ctx),
-                                   (const double*)P->pre_exact.as<double>(), T, s,
-                                   (const double*)ctx->rows.as<double>(), (const int*)ctx->reps.as<int>(), n,
-                                   (const double*)state_rows, ctx->raw.as<double>(), (const double*)zx_state,
-                                   tail, (const int*)nullptr));
-      }
+      k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(
+          lstm_weights(ctx), P->pre_exact.as<double>(), T, s, nullptr, nullptr, n, state_rows,
+          ctx->raw.as<double>(), zx_state, tail, nullptr, cr);
       TS_LAUNCHED();
       const double tw0 = trace ? now_us() : 0.0;
       // poll the result; every few thousand spins ask the stream whether it
@@ -1655,6 +1657,10 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   if (rng_state && epsilon > 0.0) *rng_state = rng;
   *visited = vis;
   if (out_best_v) *out_best_v = best_v;
+  if (fused_layers) {  // distinct children rows per layer, after the search
+    k_greedy_distinct<<<T, 256, 0, ctx->stream>>>(ghash, gcount, kMaxChildren, ctx->gstat.as<unsigned long long>());
+    TS_LAUNCHED();
+  }
   TS_CUDA(cudaMemcpyAsync(&ctx->greedy_distinct, ctx->gstat.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
