@@ -914,12 +914,14 @@ TS_HD int64_t enumerate_candidates(const StageDesc& s, const StageDesc* cs, cons
           uint8_t base[TS_MAX_LOOPS];
           int64_t bext[TS_MAX_LOOPS];
           int t = 0;
+          // t < nl <= TS_MAX_LOOPS (checked above); the bound is restated in
+          // the loops so the compiler's range analysis sees it too
           if (pl == 0) {
-            for (int j = 0; j < np; ++j) { base[t] = pure_ids[j]; bext[t++] = pure_ext[j]; }
-            for (int r = 0; r < n_red; ++r) { base[t] = (uint8_t)(8 + r); bext[t++] = s.ext[n_pure + r]; }
+            for (int j = 0; j < np && t < TS_MAX_LOOPS; ++j) { base[t] = pure_ids[j]; bext[t++] = pure_ext[j]; }
+            for (int r = 0; r < n_red && t < TS_MAX_LOOPS; ++r) { base[t] = (uint8_t)(8 + r); bext[t++] = s.ext[n_pure + r]; }
           } else {
-            for (int r = 0; r < n_red; ++r) { base[t] = (uint8_t)(8 + r); bext[t++] = s.ext[n_pure + r]; }
-            for (int j = 0; j < np; ++j) { base[t] = pure_ids[j]; bext[t++] = pure_ext[j]; }
+            for (int r = 0; r < n_red && t < TS_MAX_LOOPS; ++r) { base[t] = (uint8_t)(8 + r); bext[t++] = s.ext[n_pure + r]; }
+            for (int j = 0; j < np && t < TS_MAX_LOOPS; ++j) { base[t] = pure_ids[j]; bext[t++] = pure_ext[j]; }
           }
           for (int sw = 0; sw < 2; ++sw) {
             uint8_t seq[TS_MAX_LOOPS];
