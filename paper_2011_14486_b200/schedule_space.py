@@ -134,6 +134,7 @@ class _PipelineInfo:
         # so equal decisions built by any caller (a foreign search's own
         # objects) encode once; bounded by the distinct actions per stage
         self.val_cache = {}
+        self.dec_cache = {}   # (schedule index, record bytes) -> decision
 
     def loop_table(self, st, split):
         table = {}
@@ -215,21 +216,38 @@ class _PipelineInfo:
         return _REC.pack(*sp, *order, len(d.order), d.vectorize_width, flags, anchor)
 
     def decode(self, idx: int, rec) -> LayerSchedule:
+        """The decision a 16-byte record encodes at schedule index idx."""
+        return self.decode_bytes(idx, rec.tobytes())
+
+    def decode_bytes(self, idx: int, b: bytes) -> LayerSchedule:
+        # decisions are frozen dataclasses: one object per (index, record),
+        # shared by every caller (greedy/beam results, candidate_actions)
+        key = (idx, b)
+        d = self.dec_cache.get(key)
+        if d is not None:
+            return d
+        f = _REC.unpack(b)
         st = self.stages[idx]
         split = {}
         splits = []
         for k, (dname, _) in enumerate(st.dims):
-            f = int(rec["split"][k])
-            if f:
-                split[dname] = f
-                splits.append((dname, f))
+            if f[k]:
+                split[dname] = f[k]
+                splits.append((dname, f[k]))
         inv = {v: k for k, v in self.loop_table(st, split).items()}
-        order = tuple(inv[int(x)] for x in rec["order"][: int(rec["n_loops"])])
-        anchor = int(rec["anchor"])
+        order = tuple(inv[x] for x in f[4:4 + f[12]])
+        vec, flags, anchor = f[13], f[14], f[15]
         at = None if anchor < 0 else (self.sole[idx], anchor)
-        store = at if (int(rec["flags"]) & FLAG_STORE_AT) else None
-        return LayerSchedule(st.name, tuple(splits), order, int(rec["vec"]),
-                             bool(int(rec["flags"]) & FLAG_PARALLEL), at, store)
+        store = at if (flags & FLAG_STORE_AT) else None
+        d = LayerSchedule(st.name, tuple(splits), order, vec, bool(flags & FLAG_PARALLEL), at, store)
+        if len(self.dec_cache) < (1 << 20):
+            self.dec_cache[key] = d
+        return d
+
+    def decode_records(self, recs, start: int = 0) -> tuple:
+        """Decisions of consecutive schedule indices start.. from a record array."""
+        b = np.ascontiguousarray(recs).tobytes()
+        return tuple(self.decode_bytes(start + i, b[16 * i:16 * i + 16]) for i in range(len(b) // 16))
 
     def records_of(self, s) -> bytes:
         cached = getattr(s, "_cache", None)
@@ -407,9 +425,11 @@ def candidate_actions(s):
     out = []
     if len(inf.enc_cache) >= (1 << 20):
         inf.enc_cache.clear()
-    for r in buf[: n.value]:
-        d = inf.decode(idx, r)
-        inf.enc_cache[id(d)] = (d, r.tobytes(), idx)
+    raw = buf[: n.value].tobytes()
+    for i in range(n.value):
+        rb = raw[16 * i:16 * i + 16]
+        d = inf.decode_bytes(idx, rb)
+        inf.enc_cache[id(d)] = (d, rb, idx)
         out.append(d)
     return out
 

@@ -165,7 +165,7 @@ def greedy_schedule_gpu(p, params, noise: NoiseConfig | None = None,
     if rng is not None and eps > 0:
         rng.state = st.value
     # the chosen records are exactly the encoding of the decoded decisions
-    s = ScheduleState(p, tuple(inf.decode(i, rec) for i, rec in enumerate(out)))
+    s = ScheduleState(p, inf.decode_records(out))
     s._cache["ts_records"] = out.tobytes()
     if return_value:
         return s, visited.value, best_v.value
@@ -216,8 +216,7 @@ def beam_search_gpu(prefix, params, width: int = 8, device=None, return_value=Fa
         ctx.check(ctx.lib.ts_beam(ctx.h, pid, _lib._p(pre) if len(pre) else None, len(pre), int(width),
                                   _lib._p(out), ctypes.byref(visited), ctypes.byref(best_v)))
     d = len(prefix.decisions)
-    s = ScheduleState(p, tuple(prefix.decisions) + tuple(inf.decode(i, rec) for i, rec in enumerate(out)
-                                                         if i >= d))
+    s = ScheduleState(p, tuple(prefix.decisions) + inf.decode_records(out[d:], d))
     s._cache["ts_records"] = out.tobytes()
     if return_value:
         return s, best_v.value
