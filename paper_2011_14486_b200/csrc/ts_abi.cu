@@ -1492,6 +1492,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   auto now_us = [] {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
+  const double t_call = trace ? now_us() : 0.0;
   int64_t vis = 0;
   double best_v = 0.0;
   for (int i = 0; i < T; ++i) {
@@ -1653,7 +1654,9 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     TS_CUDA(cudaMemcpyAsync(state_rows + (int64_t)s * F, ctx->rows.as<double>() + (int64_t)best * F,
                             sizeof(double) * F, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  if (trace) fprintf(stderr, "ts_greedy: T %d, host enumeration %.0f us, waiting on the device %.0f us\n", T, t_enum, t_wait);
+  if (trace)
+    fprintf(stderr, "ts_greedy: T %d, host enumeration %.0f us, waiting on the device %.0f us, layer loop %.0f us\n", T,
+            t_enum, t_wait, now_us() - t_call);
   if (rng_state && epsilon > 0.0) *rng_state = rng;
   *visited = vis;
   if (out_best_v) *out_best_v = best_v;
