@@ -334,3 +334,31 @@ def test_exact_leg_bitwise_on_device_generated_states(gpu_ctx, v0_path, v0, net)
     decs = [[O.as_act(inf.decode(k, r)) for k, r in enumerate(hr[ho[i]:ho[i + 1]])] for i in range(n)]
     want = O.values(oracle_params(v0_path), O.Pipe(p), decs)
     assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("key", ["assets/pipelines/nets/crp2d.pl", "assets/pipelines/nets/vgg16.pl"])
+def test_greedy_stats_distinct_rows(greedy_golden, v0, key):
+    """ts_greedy_stats after the one-kernel greedy layers (distinct children
+    rows from the layers' row hashes, k_greedy_distinct) equals a bitwise
+    count: along the golden schedule, every layer's children featurized and
+    normalized on the device (featurize_states), distinct new rows counted
+    in numpy; visited equals the candidate total."""
+    import ctypes
+    from paper_2011_14486_b200.featurizer import featurize_states
+    g = greedy_golden[key]
+    p = pipeline_from(g)
+    s, visited = greedy_schedule_gpu(p, v0)
+    ctx = _lib.context(0)
+    vis, distinct = ctypes.c_int64(), ctypes.c_int64()
+    ctx.check(ctx.lib.ts_greedy_stats(ctx.h, ctypes.byref(vis), ctypes.byref(distinct)))
+    T = ss._info(p).T
+    want, total = 0, 0
+    st = ss.initial_state(p)
+    for i, r in enumerate(g["schedule"]):
+        kids = [ss.child_state(st, a) for a in ss.candidate_actions(st)]
+        total += len(kids)
+        rows = [m[T - 1 - i].tobytes() for m in featurize_states(kids, params=v0, normalized=True)]
+        want += len(set(rows))
+        st = ss.apply(st, ss.parse_layer_schedule(r))
+    assert vis.value == visited == total == g["visited"]
+    assert distinct.value == want
