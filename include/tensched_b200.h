@@ -223,9 +223,12 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
               ts_decision* out_decisions, int64_t* visited, double* out_best_v);
 
 /* Dedup statistics of the last ts_greedy call on this context: candidates
- * visited and distinct children feature rows among them (children with
- * bit-identical rows share one exact LSTM; visited / distinct is the dedup
- * factor). */
+ * visited and distinct children feature rows among them (visited / distinct
+ * is the dedup factor).  With H = 32 every child runs its own exact LSTM in
+ * the one-kernel layer (identical rows give identical V, so the argmin is
+ * unaffected) and the distinct count comes from the rows' 64-bit hashes
+ * after the search; otherwise children with bit-identical rows share one
+ * LSTM and the count is exact. */
 int ts_greedy_stats(ts_ctx* ctx, int64_t* visited, int64_t* distinct);
 
 /* One layer step for an arbitrary parent state (the children

@@ -75,3 +75,22 @@ for env in ({}, {"TS_ONE_LANE": "1"}, {"TS_CODED_STEP": str(1 << 19)}, {"TS_CODE
         os.environ.pop(k, None)
     os.environ.update(env)
     print(f"e2e coded {env or 'default'}: {timed(coded)} ms")
+
+# kernel-time sums inside one e2e call (per-kernel CUDA events on each lane):
+# if they add up to the device-resident call's, the gap is idle time
+for k in ("TS_ONE_LANE", "TS_CODED_STEP", "TS_CODED_CHUNK"):
+    os.environ.pop(k, None)
+_t = np.zeros(4)
+_c = np.zeros(4, dtype=np.int64)
+for name, fn in (("device", dev_codes), ("e2e", coded)):
+    fn()
+    torch.cuda.synchronize()
+    ctx.lib.ts_kernel_times(ctx.h, _lib._p(_t), _lib._p(_c), 1)
+    ctx.lib.ts_set_timing(ctx.h, 1)
+    t0 = time.perf_counter()
+    fn()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3
+    ctx.lib.ts_set_timing(ctx.h, 0)
+    ctx.lib.ts_kernel_times(ctx.h, _lib._p(_t), _lib._p(_c), 1)
+    print(f"{name}: wall {wall:.2f} ms, featurize/lstm/other/... ms {np.round(_t, 3)} counts {_c}")
