@@ -156,6 +156,7 @@ struct ts_ctx {
   DevBuf bk_X, bk_meta, bk_P;  // ts_lstm_backward: the batch, its layout, params + gradient
   DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
   DevBuf ghash;                 // ts_greedy: per-layer children row hashes [T][4096] + counts [T]
+  ChildRow child_row{};         // ts_greedy: the fused layer's launch parameters
   DevBuf trc_img;               // TS_TRAIN_TCF: per-step packed weight images
   bool trc_attr_set = false;
   DevBuf beam_rows;             // ts_beam: frontier state rows, double-buffered
@@ -1527,10 +1528,14 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       // in, and the last block to finish runs the argmin, installs the
       // winner's row and writes the layer's result into mapped host memory,
       // which the host polls (no copy, no stream sync)
-      ChildRow cr;
+      ChildRow& cr = ctx->child_row;  // ~3.5 KB: kept in the context, not on the stack per layer
       cr.P = P->d.as<PipelineDesc>();
       cr.cands = hs;
       cr.cnest = cn ? hn : nullptr;
+      cr.n_inline = n <= kInlineCands ? n : 0;
+      cr.has_nest = cn != nullptr;
+      if (cn) cr.nest = *cn;
+      if (cr.n_inline) memcpy(cr.c, cands.data(), sizeof(ts_decision) * n);
       cr.init_raw = P->init_raw.as<double>();
       cr.mean = ctx->mean.as<double>();
       cr.stdv = ctx->stdv.as<double>();
