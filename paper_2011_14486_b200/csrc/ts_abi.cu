@@ -1534,6 +1534,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       cr.cnest = cn ? hn : nullptr;
       cr.n_inline = n <= kInlineCands ? n : 0;
       cr.has_nest = cn != nullptr;
+      cr.consumer = sd.consumer;
       if (cn) cr.nest = *cn;
       if (cr.n_inline) memcpy(cr.c, cands.data(), sizeof(ts_decision) * n);
       cr.init_raw = P->init_raw.as<double>();
