@@ -64,8 +64,9 @@ def parse_args():
     ap.add_argument("--no-greedy", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-pairs", type=int, default=10_000_000, help="training pairs per GPU")
-    ap.add_argument("--train-batch", type=int, default=16384,
-                    help="per-GPU minibatch (128 tensor-core tiles: about one per SM)")
+    ap.add_argument("--train-batch", type=int, default=0,
+                    help="per-GPU minibatch; 0 = 128 x the SM count (one 128-sequence tensor-core tile "
+                         "per SM: 18,944 on a B200)")
     ap.add_argument("--big-states", type=int, default=100_000_000,
                     help="single-GPU sweep point (configs[3]'s 1e8 states on one GPU; 0 = skip)")
     ap.add_argument("--no-ref-greedy", action="store_true",
@@ -397,7 +398,7 @@ def train_throughput(ctx, pid, inf, params, rank, world, dev, args):
     g = DeviceGradients.from_device(ctx, rows.data_ptr(), S * T, init.data_ptr(), T, row_base.data_ptr(),
                                     init_base.data_ptr(), Tl.data_ptr(), depth.data_ptr(),
                                     logt.data_ptr(), N, params.hidden)
-    B = args.train_batch
+    B = args.train_batch or 128 * torch.cuda.get_device_properties(dev).multi_processor_count
     rng = np.random.Generator(np.random.PCG64(1234 + rank))
     perm = rng.permutation(N).astype(np.int32)
     n_hold = min(65536, N // 10)
