@@ -1121,21 +1121,30 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
   // starts the device early; up to 2^20 states the rest goes as one batch,
   // beyond that in batches of 2^20 (each result block streams back on its
   // own stream while the next batch computes; only the last one is exposed).
+  // Beyond 2^20 states the chunks grow geometrically (x2 per chunk up to
+  // `step`): each chunk's transfer (~0.65 ns per state) then finishes within
+  // the previous chunk's compute (~1.9 ns per state), so the device never
+  // waits for bytes, while large chunks keep the per-chunk kernel tails few.
   int64_t first = n_states >= (1 << 18) ? std::min<int64_t>(n_states / 4, 1 << 18) : n_states;
-  int64_t step = 1 << 20;
+  int64_t step = 1 << 21;
   bool stepped = n_states > (1 << 20);
+  bool grow = true;
   if (const char* e = getenv("TS_CODED_CHUNK")) first = std::max<int64_t>(1024, atoll(e));
   if (const char* e = getenv("TS_CODED_STEP")) {
     step = std::max<int64_t>(1024, atoll(e));
     stepped = true;
+    grow = false;
   }
+  if (const char* e = getenv("TS_CODED_CAP")) step = std::max<int64_t>(1024, atoll(e));  // growth cap
   if (first > n_states) first = n_states;
   std::vector<int64_t> st_at = {0, first};
   if (!stepped) {
     if (first < n_states) st_at.push_back(n_states);
   } else {
+    int64_t c = first;
     for (int64_t s0 = first; s0 < n_states;) {
-      s0 = std::min(n_states, s0 + step);
+      c = grow ? std::min(step, 2 * c) : step;
+      s0 = std::min(n_states, s0 + c);
       st_at.push_back(s0);
     }
   }
@@ -1191,7 +1200,7 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
       TS_CUDA(ctx->scan_tmp.reserve(temp + 16, ctx->stream));
       if (mode == TS_MODE_FAST) {
         TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, max_chunk), ctx->stream));
-        if (rows_bound <= ((size_t)2 << 30)) TS_CUDA(ctx->rows.reserve(rows_bound, ctx->stream));
+        if (rows_bound <= ((size_t)4 << 30)) TS_CUDA(ctx->rows.reserve(rows_bound, ctx->stream));
       }
     }
   }

@@ -68,10 +68,10 @@ def coded():
 
 
 print(f"M = {M}: device records {timed(dev_step)} ms, device codes {timed(dev_codes)} ms  (median, min)")
-for env in ({}, {"TS_ONE_LANE": "1"}, {"TS_CODED_STEP": str(1 << 19)}, {"TS_CODED_STEP": str(1 << 21)},
-            {"TS_CODED_CHUNK": str(1 << 17)}, {"TS_CODED_CHUNK": str(1 << 19)},
-            {"TS_CODED_CHUNK": str(1 << 20), "TS_CODED_STEP": str(1 << 21)}):
-    for k in ("TS_ONE_LANE", "TS_CODED_STEP", "TS_CODED_CHUNK"):
+for env in ({}, {"TS_CODED_STEP": str(1 << 20)}, {"TS_CODED_CAP": str(1 << 22)},
+            {"TS_CODED_CAP": str(1 << 22), "TS_CODED_CHUNK": str(1 << 17)}, {"TS_CODED_CAP": str(3 << 20)},
+            {"TS_CODED_CHUNK": str(1 << 19)}):
+    for k in ("TS_ONE_LANE", "TS_CODED_STEP", "TS_CODED_CHUNK", "TS_CODED_CAP"):
         os.environ.pop(k, None)
     os.environ.update(env)
     print(f"e2e coded {env or 'default'}: {timed(coded)} ms")
