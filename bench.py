@@ -929,8 +929,13 @@ def main():
             s = beam_search_gpu(initial_state(pn), params, 8)
             beam[net] = {"wall_s": round(time.perf_counter() - t0, 4), "first_call_s": round(first, 4),
                          "width": 8, "schedule": [d.render() for d in s.decisions]}
-        try:
-            level1 = v_callable_rate(GOLD / "v0.ckpt")
+        try:  # in a fresh process, like a user's: this one holds the bench's
+            # buffers and objects (its collector passes and allocator state
+            # slowed the Python-side encoding ~4x)
+            import multiprocessing as mp
+            with mp.get_context("spawn").Pool(1) as pool:
+                level1 = pool.apply(v_callable_rate, (GOLD / "v0.ckpt",))
+            level1["process"] = "fresh (spawned) process, its own CUDA context"
         except Exception as e:  # reported, never silently replaced
             level1 = {"unavailable": str(e)}
         if not args.no_ref_greedy:
