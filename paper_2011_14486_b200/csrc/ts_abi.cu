@@ -127,6 +127,7 @@ struct ts_ctx {
   int sm_count = 148;
   bool tc_attr_set = false;
   bool exact_attr_set = false;
+  bool exact2_attr_set = false;
   bool tr_tc_attr_set = false;
   // optional per-kernel-class timing (bench.py): events around launches on
   // the context stream, resolved at the next host synchronization
@@ -797,9 +798,48 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
                                        (int)sizeof(ExactSmem)));
           ctx->exact_attr_set = true;
         }
-        k_score_exact32<<<(unsigned)((threads + 511) / 512), 512, sizeof(ExactSmem), ctx->stream>>>(
-            lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
-            ctx->target_scale, d_out);
+        if (n_states >= 4096 && !getenv("TS_EXACT_X1")) {
+          // depth-sorted pairs, two states per warp (k_score_exact32x2)
+          TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, n_states), ctx->stream));
+          int64_t* rowoff = ctx->reps.as<int64_t>();
+          int* perm = reinterpret_cast<int*>(rowoff + (T + 2));
+          int* hist = perm + n_states;
+          int* cursor = hist + (T + 2);
+          const unsigned g = (unsigned)((n_states + 255) / 256);
+          TS_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (T + 2), ctx->stream));
+          tc::k_depth_hist<<<std::min<unsigned>(g, 4u * ctx->sm_count), 256, sizeof(int) * (T + 1),
+                             ctx->stream>>>(d_offsets, n_states, T, hist);
+          TS_LAUNCHED();
+          tc::k_depth_scan<<<1, 32, 0, ctx->stream>>>(hist, T, cursor, rowoff);
+          TS_LAUNCHED();
+          const int64_t per_block = (int64_t)tc::SCATTER_THREADS * tc::SCATTER_PER;
+          tc::k_depth_scatter<<<(unsigned)((n_states + per_block - 1) / per_block), tc::SCATTER_THREADS,
+                                sizeof(int) * 2 * (T + 1), ctx->stream>>>(d_offsets, n_states, T, cursor, perm);
+          TS_LAUNCHED();
+          const bool four = getenv("TS_EXACT_X4") != nullptr;
+          const size_t smn = four ? exact32xn_smem<4>(256) : exact32xn_smem<2>(256);
+          if (!ctx->exact2_attr_set) {
+            TS_CUDA(cudaFuncSetAttribute(k_score_exact32xn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)exact32xn_smem<2>(256)));
+            TS_CUDA(cudaFuncSetAttribute(k_score_exact32xn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)exact32xn_smem<4>(256)));
+            ctx->exact2_attr_set = true;
+          }
+          const int ns = four ? 4 : 2;
+          const int64_t warps = (n_states + ns - 1) / ns;
+          if (four)
+            k_score_exact32xn<4><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
+                lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
+                n_states, ctx->target_scale, d_out);
+          else
+            k_score_exact32xn<2><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
+                lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
+                n_states, ctx->target_scale, d_out);
+        } else {
+          k_score_exact32<<<(unsigned)((threads + 511) / 512), 512, sizeof(ExactSmem), ctx->stream>>>(
+              lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
+              ctx->target_scale, d_out);
+        }
       } else {
         k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
             lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,

@@ -455,8 +455,11 @@ __global__ void k_depth_hist(const int64_t* __restrict__ offsets, int64_t n, int
   extern __shared__ int sh[];
   for (int i = threadIdx.x; i <= T; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(sh + (int)(offsets[i + 1] - offsets[i]), 1);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = offsets[i + 1] - offsets[i];
+    // a depth outside 0..T sorts as 0 (the featurizer reports it)
+    atomicAdd(sh + (d >= 0 && d <= T ? (int)d : 0), 1);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i <= T; i += blockDim.x)
     if (sh[i]) atomicAdd(hist + i, sh[i]);
@@ -503,7 +506,8 @@ __global__ void __launch_bounds__(SCATTER_THREADS) k_depth_scatter(const int64_t
 #pragma unroll
   for (int k = 0; k < SCATTER_PER; ++k) {
     const int64_t i = b0 + k * SCATTER_THREADS + threadIdx.x;
-    dep[k] = i < n ? (int)(offsets[i + 1] - offsets[i]) : -1;
+    const int64_t d = i < n ? offsets[i + 1] - offsets[i] : -1;
+    dep[k] = i < n ? (d >= 0 && d <= T ? (int)d : 0) : -1;  // as k_depth_hist
     rank[k] = dep[k] >= 0 ? atomicAdd(cnt + dep[k], 1) : 0;
   }
   __syncthreads();

@@ -362,3 +362,42 @@ def test_greedy_stats_distinct_rows(greedy_golden, v0, key):
         st = ss.apply(st, ss.parse_layer_schedule(r))
     assert vis.value == visited == total == g["visited"]
     assert distinct.value == want
+
+
+def test_exact_sweep_kernels_agree_bitwise(gpu_ctx, v0):
+    """The exact sweep's two-states-per-warp kernel (k_score_exact32xn<2>,
+    depth-sorted pairs, batches >= 4,096) equals the one-state-per-warp
+    kernel (k_score_exact32, TS_EXACT_X1) bit for bit on 20,000
+    device-generated VGG-16 and ResNet-18 states (ragged depths, odd count:
+    the last warp holds one state)."""
+    import ctypes
+    import os
+    import pathlib
+    import torch
+    for net in ("vgg16", "resnet18"):
+        p = pipeline_from({"text": (pathlib.Path(__file__).resolve().parent.parent / "assets" / "pipelines"
+                                    / "nets" / f"{net}.pl").read_text()})
+        inf = ss._info(p)
+        n = 20_001
+        with gpu_ctx.lock:
+            gpu_ctx.set_params(v0)
+            pid = gpu_ctx.pipeline_id(inf.desc)
+            recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
+            offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            nrec = ctypes.c_int64()
+            gpu_ctx.check(gpu_ctx.lib.ts_generate_states_device(gpu_ctx.h, pid, 31337, n, recs.data_ptr(),
+                                                                offs.data_ptr(), ctypes.byref(nrec)))
+            got = {}
+            for x1 in (False, True):
+                if x1:
+                    os.environ["TS_EXACT_X1"] = "1"
+                try:
+                    o = torch.empty(n, dtype=torch.float64, device="cuda")
+                    gpu_ctx.check(gpu_ctx.lib.ts_score_states_device(gpu_ctx.h, pid, recs.data_ptr(),
+                                                                     offs.data_ptr(), n, nrec.value, MODE_EXACT,
+                                                                     o.data_ptr()))
+                    got[x1] = o.cpu().numpy()
+                finally:
+                    os.environ.pop("TS_EXACT_X1", None)
+        assert np.all(got[False] > 0)
+        assert np.array_equal(bits(got[False]), bits(got[True])), net
