@@ -1224,8 +1224,8 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
       ev.clear();
     }
   } drain{ctx, ev};
-  // FAST: chunks alternate between two lanes (the exact leg indexes its rows
-  // by global record offsets, so it stays on one lane)
+  // FAST: chunks alternate between two lanes (the exact leg, latency-free
+  // and fp64-bound, stays on one)
   const bool two_lanes = mode == TS_MODE_FAST && n_chunks > 1 && !getenv("TS_ONE_LANE");
   {  // per-lane scratch sized for the largest chunk up front, so no buffer a
      // queued kernel reads is reallocated while chunks are in flight
@@ -1238,8 +1238,9 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     for (int ln = 0; ln < (two_lanes ? 2 : 1); ++ln) {
       LaneSwap lane(ctx, ln == 1);
       TS_CUDA(ctx->scan_tmp.reserve(temp + 16, ctx->stream));
+      // depth bucketing scratch (both legs sort by depth)
+      TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, max_chunk), ctx->stream));
       if (mode == TS_MODE_FAST) {
-        TS_CUDA(ctx->reps.reserve(fast_reps_bytes(T, max_chunk), ctx->stream));
         if (rows_bound <= ((size_t)4 << 30)) TS_CUDA(ctx->rows.reserve(rows_bound, ctx->stream));
       }
     }
@@ -1267,20 +1268,22 @@ int ts_score_states_coded(ts_ctx* ctx, int pipeline_id, const uint16_t* codes, c
     ev.push_back(in);
     TS_CUDA(cudaEventRecord(in, ctx->copy_stream));
     TS_CUDA(cudaStreamWaitEvent(ctx->stream, in, 0));
-    // offsets of this chunk: off_k[0] = r0, then the scan of its depths
+    // offsets of this chunk, chunk-local (off_k[0] = 0, then the scan of its
+    // depths); its codes are read from d_codes + r0
     int64_t* off_k = d_off + s0 + k;
     k_depths_to_counts<<<(unsigned)((s1 - s0 + 255) / 256), 256, 0, ctx->stream>>>(d_depth + s0, s1 - s0,
-                                                                                     off_k, r0);
+                                                                                     off_k, 0);
     TS_LAUNCHED();
     size_t temp = 0;
     TS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
     TS_CUDA(ctx->scan_tmp.reserve(temp + 16, ctx->stream));
     TS_CUDA(cub::DeviceScan::InclusiveSum(ctx->scan_tmp.p, temp, off_k + 1, off_k + 1, s1 - s0, ctx->stream));
     ++ctx->launches;
-    // FAST rows are chunk-local (decision-major by rowoff); the exact leg's
-    // are indexed by global record offsets
-    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), off_k, s1 - s0,
-                      mode == TS_MODE_FAST ? r1 - r0 : r1, mode, ctx->out.as<double>() + s0, d_codes);
+    // rows are chunk-local in both legs (FAST: decision-major by rowoff;
+    // exact: by the chunk-local record offsets), so scratch scales with the
+    // largest chunk, not with the batch
+    rc = score_device(ctx, P, P->code_table.as<ts_decision>(), off_k, s1 - s0, r1 - r0, mode,
+                      ctx->out.as<double>() + s0, d_codes + r0);
     if (rc) return rc;
     cudaEvent_t done = take_event(ctx);
     ev.push_back(done);
