@@ -770,9 +770,13 @@ static int resolve_mode(ts_ctx* ctx, PipelineSlot* P, int& mode) {
 }
 
 // d_codes (optional): 16-bit action codes instead of records, same offsets
+// n_records: records of this batch (offsets[n] - offsets[0]); rec_base =
+// offsets[0] (callers scoring a chunk of a larger batch keep its absolute
+// offsets): the exact leg's rows are indexed from it, so its scratch is the
+// chunk's, not the batch's
 static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_records,
                         const int64_t* d_offsets, int64_t n_states, int64_t n_records, int mode,
-                        double* d_out, const uint16_t* d_codes = nullptr) {
+                        double* d_out, const uint16_t* d_codes = nullptr, int64_t rec_base = 0) {
   int rc = ensure_pipe_ready(ctx, P);
   if (rc) return rc;
   const int T = P->h->n_stages;
@@ -783,7 +787,7 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
       k_featurize_rows<double><<<(unsigned)((n_states + 127) / 128), 128, slot_smem(P, 128), ctx->stream>>>(
           P->d.as<PipelineDesc>(), d_records, d_offsets, n_states, P->init_norm.as<double>(),
           ctx->mean.as<double>(), ctx->stdv.as<double>(), ctx->rows.as<double>(), ctx->status.as<int>(),
-          nullptr, nullptr, d_codes);
+          nullptr, nullptr, d_codes, nullptr, rec_base);
       TS_LAUNCHED();
     }
     {
@@ -830,20 +834,20 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
           if (four)
             k_score_exact32xn<4><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
                 lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
-                n_states, ctx->target_scale, d_out);
+                n_states, ctx->target_scale, d_out, rec_base);
           else
             k_score_exact32xn<2><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
                 lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
-                n_states, ctx->target_scale, d_out);
+                n_states, ctx->target_scale, d_out, rec_base);
         } else {
           k_score_exact32<<<(unsigned)((threads + 511) / 512), 512, sizeof(ExactSmem), ctx->stream>>>(
               lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
-              ctx->target_scale, d_out);
+              ctx->target_scale, d_out, rec_base);
         }
       } else {
         k_score_exact<<<(unsigned)((threads + 255) / 256), 256, 0, ctx->stream>>>(
             lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
-            ctx->target_scale, d_out);
+            ctx->target_scale, d_out, rec_base);
       }
       TS_LAUNCHED();
     }
@@ -1015,8 +1019,8 @@ int ts_score_states(ts_ctx* ctx, int pipeline_id, const ts_decision* records, co
   for (int64_t k = 0; k < n_chunks; ++k) {
     const int64_t s0 = k * chunk, s1 = std::min(n_states, s0 + chunk);
     TS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[k], 0));
-    rc = score_device(ctx, P, d_rec, ctx->offsets.as<int64_t>() + s0, s1 - s0, n_rec, mode,
-                      ctx->out.as<double>() + s0);
+    rc = score_device(ctx, P, d_rec, ctx->offsets.as<int64_t>() + s0, s1 - s0, offsets[s1] - offsets[s0], mode,
+                      ctx->out.as<double>() + s0, nullptr, offsets[s0]);
     if (rc) return rc;
     TS_CUDA(cudaMemcpyAsync(out_v + s0, ctx->out.as<double>() + s0, sizeof(double) * (s1 - s0),
                             cudaMemcpyDeviceToHost, ctx->stream));
@@ -1128,7 +1132,7 @@ int ts_score_states_packed(ts_ctx* ctx, int pipeline_id, const uint64_t* packed,
       k_unpack<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, ctx->stream>>>(d_packed + r0, r1 - r0, d_rec + r0);
       TS_LAUNCHED();
     }
-    rc = score_device(ctx, P, d_rec, d_off + s0, s1 - s0, n_rec, mode, ctx->out.as<double>() + s0);
+    rc = score_device(ctx, P, d_rec, d_off + s0, s1 - s0, r1 - r0, mode, ctx->out.as<double>() + s0, nullptr, r0);
     if (rc) return rc;
     TS_CUDA(cudaMemcpyAsync(out_v + s0, ctx->out.as<double>() + s0, sizeof(double) * (s1 - s0),
                             cudaMemcpyDeviceToHost, ctx->stream));
