@@ -801,10 +801,10 @@ def main():
     avg = {names[k]: times[k] / counts[k] for k in range(4) if counts[k]}
     dom = max(avg, key=lambda k: times[names.index(k)])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    # ncu --set full captures (profiles/r01_ncu.md): DRAM bytes per state of each
+    # ncu --set full captures (profiles/r02_ncu.md): DRAM bytes per state of each
     # kernel at 12.5M states (this bench's default launch), scaled to this launch
-    traffic_per_state = {"featurize": (6.281158e9 + 6.988932e9) / 12.5e6,
-                         "lstm_fast": (8.768533e9 + 0.394084e9) / 12.5e6}
+    traffic_per_state = {"featurize": (6.277518e9 + 6.988419e9) / 12.5e6,
+                         "lstm_fast": (8.762989e9 + 0.379514e9) / 12.5e6}
     row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
         # SURVEY 8(d)'s per-unit figure: decision records read (32 B per
@@ -826,15 +826,23 @@ def main():
                 "physical": {"bytes_per_launch": phys, "achieved_gbs": phys / (avg[dom] / 1e3) / 1e9,
                              "what": f"16 B record read + {row_bytes} B row written per scheduled stage"}}
     else:
-        flops_per_launch = FLOPS_PER_STEP * timesteps
+        # SURVEY 8(d)'s per-unit figure: 12,352 flops per state-timestep over
+        # the full state (T timesteps); the kernel executes only the
+        # scheduled timesteps (the shared unscheduled prefix is computed once
+        # per pipeline): `executed`
+        flops_per_launch = FLOPS_PER_STEP * T * M
         achieved = flops_per_launch / (avg[dom] / 1e3) / 1e12
+        executed = FLOPS_PER_STEP * timesteps
         peak = peaks.get("bf16_tflops", 1590.0)
         tr = traffic_per_state.get(dom)
         roof = {"kernel": "k_lstm_tc" if dom == "lstm_fast" else "k_score_exact", "bound": "tensor",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": tr * M if tr else None, "traffic_source": TRAFFIC_SOURCE,
                 "flops_per_launch": flops_per_launch,
-                "algorithmic": "12352 flops per state-timestep x scheduled timesteps"}
+                "algorithmic": "SURVEY 8(d): 12352 flops per state-timestep x T timesteps per state",
+                "executed": {"flops_per_launch": executed,
+                             "achieved_tflops": executed / (avg[dom] / 1e3) / 1e12,
+                             "what": "scheduled timesteps only (shared unscheduled prefix computed once)"}}
     roof["kernel_ms"] = {k: round(v, 4) for k, v in avg.items()}
     if "lstm_fast" in avg:
         # the LSTM's binding unit: 5 ex2 + 1 rcp per hidden unit and
@@ -849,20 +857,20 @@ def main():
     if "featurize" in avg and mode == _lib.MODE_FAST:
         # the featurizer's binding resource is instruction issue (integer
         # walk): warp instructions per scheduled row from the ncu capture
-        # (9.3225e9 warp instructions for 12.5M states = 218.7M rows),
-        # against 4 warp instructions / clk / SM
+        # (7.6023e9 warp instructions for 12.5M states = 218.7M rows,
+        # profiles/r02_ncu.md), against 4 warp instructions / clk / SM
         mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965
         issue_peak = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * mhz * 1e6
-        issued = 9.322507e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
+        issued = 7.602255e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
         roof["k_featurize_rows_issue"] = {"bound": "issue", "achieved": issued / 1e12, "peak": issue_peak / 1e12,
                                           "unit": "T warp-instr/s", "frac": issued / issue_peak,
-                                          "algorithmic": "42.6 warp instructions per scheduled row (ncu)",
+                                          "algorithmic": "34.8 warp instructions per scheduled row (ncu)",
                                           "instructions_source": "constant from one ncu --set full "
-                                                                 "capture (profiles/r01_ncu.md), not "
+                                                                 "capture (profiles/r02_ncu.md), not "
                                                                  "measured in this run"}
-    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 79%, "
-                    "issue 59% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work "
-                    "(ALU 58%, issue 67%); profiles/r01_ncu.md")
+    roof["note"] = ("neither kernel is HBM- or tensor-bound: k_lstm_tc is MUFU/issue-bound (XU pipe 83%, "
+                    "issue 61% in ncu; k_lstm_tc_mufu), k_featurize_rows is ALU/issue-bound integer work; "
+                    "profiles/r02_ncu.md")
 
     # ---- batch-size sweep (1e4..1e7 states per GPU), device-resident,
     # on prefixes of this rank's states: where launch latency stops mattering

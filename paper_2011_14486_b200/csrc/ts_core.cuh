@@ -772,8 +772,29 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
   return nullptr;
 }
 
+#ifdef __CUDA_ARCH__
+// log2 of a nonzero 256-bit integer to float accuracy: bit length from the
+// leading word, top 32 bits as the mantissa, one MUFU lg2 (|error| < 2^-21).
+// The tensor-core (FAST) leg's recompute and invocation features only: its
+// operands are rounded to f32 and split into 22-bit fp16 pairs anyway.
+__device__ __forceinline__ double fast_log2_u256(const u256& a) {
+  // leading word by selects (a dynamic a.w[k] would put the value in local memory)
+  const int k = a.w[3] ? 3 : a.w[2] ? 2 : a.w[1] ? 1 : 0;
+  const uint64_t hi = k == 3 ? a.w[3] : k == 2 ? a.w[2] : k == 1 ? a.w[1] : a.w[0];
+  const uint64_t lo = k == 3 ? a.w[2] : k == 2 ? a.w[1] : k == 1 ? a.w[0] : 0;
+  const int lz = __clzll((long long)hi);
+  const uint64_t top = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;  // leading 1 at bit 63
+  const int e = 64 * k + 63 - lz;
+  const float m = (float)(uint32_t)(top >> 32) * 4.656612873077393e-10f;  // [1, 2)
+  return (double)e + (double)__log2f(m);
+}
+#endif
+
 // Acquired features f8..f15 of a scheduled stage (featurizer.py:86-103),
-// raw (not normalized).
+// raw (not normalized).  kFast (device, tensor-core leg only): f13 and f15
+// to float accuracy (fast_log2_u256) instead of the correctly rounded
+// division and glibc's log2 - see k_featurize_rows<float>.
+template <bool kFast = false>
 TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe, const ts_decision& d,
                             double* f, uint32_t inner) {
   f[0] = 1.0;
@@ -786,6 +807,24 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
 #pragma unroll
   for (int k = 0; k < TS_MAX_PURE; ++k)
     if (k < s.n_pure) region *= (uint64_t)pe[k];
+#ifdef __CUDA_ARCH__
+  if constexpr (kFast) {
+    // log2(inv * ppi / domain_points) = log2(inv) + log2(ppi) - log2(dp);
+    // equal numerator and denominator (recompute 1) still give exactly 0
+    u256 num = n.inv;
+    bool ok = u256_mul_u64(num, region);
+    ok = u256_mul_u64(num, s.red_points) && ok;
+    if (!ok) return TS_ERR_OVERFLOW;
+    const u256 den = u256_from(s.domain_points);
+    f[5] = fast_log2_u256(num) - fast_log2_u256(den);
+    const uint64_t pts = (d.flags & TS_FLAG_STORE_AT) ? region : s.pure_points;
+    f[6] = pts <= 8192u ? 1.0 : 0.0;
+    u256 inv1 = n.inv;
+    if (!u256_add_u64(inv1, 1)) return TS_ERR_OVERFLOW;
+    f[7] = (u256_small(inv1) && inv1.w[0] < (uint64_t)LOG2_TABLE) ? log2_int(inv1.w[0]) : fast_log2_u256(inv1);
+    return TS_OK;
+  }
+#endif
   // inv * ppi below 2^128 (all but the deepest anchor chains): one
   // branch-uniform 128-bit correctly rounded division
   bool fit = n.inv.w[2] == 0 && n.inv.w[3] == 0;
