@@ -619,6 +619,8 @@ int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* p
     if (sd.domain_points == 0) return fail(ctx, TS_ERR_PIPELINE, "empty domain");
     sd.dp = make_divisor(sd.domain_points);
     sd.io = make_divisor(1 + sd.i_in_bytes + sd.i_out_bytes);
+    // FAST leg's f13 = log2(inv) + log2(region) + log2(red_points / domain_points)
+    sd.fast_c13 = std::log2((double)sd.red_points) - std::log2((double)sd.domain_points);
     if (sd.consumer >= T || sd.slot >= n_slots || (sd.consumer >= 0 && sd.consumer <= s))
       return fail(ctx, TS_ERR_PIPELINE, "bad consumer/slot");
   }

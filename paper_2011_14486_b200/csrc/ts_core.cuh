@@ -450,6 +450,7 @@ struct StageDesc {
   int64_t cwindow[2][TS_MAX_PURE];
   int32_t slot;  // nest slot (static liveness allocation), -1 = nest never read
   int32_t n_splittable;  // splittable pure dims: innermost two (schedule_space.py:399)
+  double fast_c13;       // log2(red_points) - log2(domain_points) (FAST leg's f13, host libm)
 };
 
 struct PipelineDesc {
@@ -773,6 +774,13 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
 }
 
 #ifdef __CUDA_ARCH__
+// log2 of a nonzero 64-bit integer to float accuracy (see fast_log2_u256)
+__device__ __forceinline__ double fast_log2_u64(uint64_t v) {
+  const int lz = __clzll((long long)v);
+  const float m = (float)(uint32_t)((v << lz) >> 32) * 4.656612873077393e-10f;  // [1, 2)
+  return (double)(63 - lz) + (double)__log2f(m);
+}
+
 // log2 of a nonzero 256-bit integer to float accuracy: bit length from the
 // leading word, top 32 bits as the mantissa, one MUFU lg2 (|error| < 2^-21).
 // The tensor-core (FAST) leg's recompute and invocation features only: its
@@ -809,14 +817,17 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
     if (k < s.n_pure) region *= (uint64_t)pe[k];
 #ifdef __CUDA_ARCH__
   if constexpr (kFast) {
-    // log2(inv * ppi / domain_points) = log2(inv) + log2(ppi) - log2(dp);
-    // equal numerator and denominator (recompute 1) still give exactly 0
-    u256 num = n.inv;
-    bool ok = u256_mul_u64(num, region);
-    ok = u256_mul_u64(num, s.red_points) && ok;
-    if (!ok) return TS_ERR_OVERFLOW;
-    const u256 den = u256_from(s.domain_points);
-    f[5] = fast_log2_u256(num) - fast_log2_u256(den);
+    // log2(inv * region * red_points / domain_points): the logs of inv and
+    // region plus the stage's constant log2(red_points / domain_points).
+    // The product is formed (to report an overflow as the exact leg does)
+    // only when its bit length could exceed 256
+    if (u256_bitlen(n.inv) + (64 - __clzll((long long)region)) + (64 - __clzll((long long)s.red_points)) > 256) {
+      u256 num = n.inv;
+      bool ok = u256_mul_u64(num, region);
+      ok = u256_mul_u64(num, s.red_points) && ok;
+      if (!ok) return TS_ERR_OVERFLOW;
+    }
+    f[5] = fast_log2_u256(n.inv) + fast_log2_u64(region) + s.fast_c13;
     const uint64_t pts = (d.flags & TS_FLAG_STORE_AT) ? region : s.pure_points;
     f[6] = pts <= 8192u ? 1.0 : 0.0;
     u256 inv1 = n.inv;
