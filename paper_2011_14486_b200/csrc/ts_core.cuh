@@ -500,13 +500,27 @@ TS_HD bool anchor_ok(const Nest& c, int lvl) {
 // Per-invocation pure extents, invocations and depth of stage `s` anchored
 // at level `lvl` of its sole consumer's nest (schedule_space.py:190-225).
 // Returns TS_OK / TS_ERR_OVERFLOW.
-template <class CN>
+// kFast (device, tensor-core leg): invocations carried as a double in
+// inv.w[0] (exact below 2^53, float-accurate beyond - they feed only the
+// FAST leg's f13/f15 logarithms, see acquired_features<true>)
+template <bool kFast = false, class CN>
 TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn, int lvl,
                            int64_t* pe, u256& inv, int& depth) {
   // invocations = consumer invocations * prod(outer loop extents up to lvl);
   // a 128-bit path covers all but the deepest chains (branch-uniform within
   // a warp far more often than a 64/256 split), 256 bits the rest
   bool ok = true;
+#ifdef __CUDA_ARCH__
+  if constexpr (kFast) {
+    double v = __longlong_as_double((long long)cn.inv_w(0));
+#pragma unroll
+    for (int j = 0; j < TS_MAX_LOOPS; ++j)
+      if (j <= lvl && j < cn.loops()) v *= (double)cn.ext_at(j);
+    inv.w[0] = (uint64_t)__double_as_longlong(v);
+    inv.w[1] = inv.w[2] = inv.w[3] = 0;
+    ok = v < 1.157920892373162e77;  // 2^256: the exact leg's overflow bound
+  } else
+#endif
   {
     unsigned __int128 p = ((unsigned __int128)cn.inv_w(1) << 64) | cn.inv_w(0);
     bool fit = cn.inv_w(2) == 0 && cn.inv_w(3) == 0;
@@ -576,17 +590,17 @@ TS_HD int anchored_extents(const StageDesc& s, const StageDesc& cs, const CN& cn
 // inner_out (optional): the innermost loop's extent, taken from the value
 // being stored (a later lookup ext[n_loops - 1] is a dynamic index, which
 // would pin the Nest in local memory on the device).
-template <class CN = Nest>
+template <bool kFast = false, class CN = Nest>
 TS_HD int build_nest(const StageDesc& s, const StageDesc* cs, const CN* cn, const ts_decision& d,
                      Nest& out, int64_t* pe, uint32_t* inner_out = nullptr) {
   if (d.anchor >= 0) {
     if (!cn || !cs || d.anchor >= cn->loops()) return TS_ERR_ILLEGAL;
-    const int rc = anchored_extents(s, *cs, *cn, d.anchor, pe, out.inv, out.depth);
+    const int rc = anchored_extents<kFast>(s, *cs, *cn, d.anchor, pe, out.inv, out.depth);
     if (rc) return rc;
   } else {
 #pragma unroll
     for (int k = 0; k < TS_MAX_PURE; ++k) pe[k] = s.ext[k];
-    out.inv = u256_from(1);
+    out.inv = u256_from(kFast ? 0x3FF0000000000000ull : 1);  // kFast: 1.0 as a double
     out.depth = 0;
   }
   if (d.n_loops == 0 || d.n_loops > TS_MAX_LOOPS) return TS_ERR_ILLEGAL;
@@ -774,6 +788,15 @@ inline const char* check_decision(const StageDesc& s, const StageDesc* cs, const
 }
 
 #ifdef __CUDA_ARCH__
+// log2 of a positive finite double to float accuracy: its exponent plus
+// one MUFU lg2 of its mantissa
+__device__ __forceinline__ double fast_log2_d(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  const int e = (int)((b >> 52) & 0x7FF) - 1023;
+  const float m = (float)__longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+  return (double)e + (double)__log2f(m);
+}
+
 // log2 of a nonzero 64-bit integer to float accuracy (see fast_log2_u256)
 __device__ __forceinline__ double fast_log2_u64(uint64_t v) {
   const int lz = __clzll((long long)v);
@@ -817,22 +840,16 @@ TS_HD int acquired_features(const StageDesc& s, const Nest& n, const int64_t* pe
     if (k < s.n_pure) region *= (uint64_t)pe[k];
 #ifdef __CUDA_ARCH__
   if constexpr (kFast) {
-    // log2(inv * region * red_points / domain_points): the logs of inv and
-    // region plus the stage's constant log2(red_points / domain_points).
-    // The product is formed (to report an overflow as the exact leg does)
-    // only when its bit length could exceed 256
-    if (u256_bitlen(n.inv) + (64 - __clzll((long long)region)) + (64 - __clzll((long long)s.red_points)) > 256) {
-      u256 num = n.inv;
-      bool ok = u256_mul_u64(num, region);
-      ok = u256_mul_u64(num, s.red_points) && ok;
-      if (!ok) return TS_ERR_OVERFLOW;
-    }
-    f[5] = fast_log2_u256(n.inv) + fast_log2_u64(region) + s.fast_c13;
+    // invocations as a double (anchored_extents<true>); log2(inv * region *
+    // red_points / domain_points) = log2(inv) + log2(region) + the stage's
+    // constant log2(red_points / domain_points)
+    const double inv = __longlong_as_double((long long)n.inv.w[0]);
+    if (!(inv * (double)region * (double)s.red_points < 1.157920892373162e77)) return TS_ERR_OVERFLOW;
+    f[5] = fast_log2_d(inv) + fast_log2_u64(region) + s.fast_c13;
     const uint64_t pts = (d.flags & TS_FLAG_STORE_AT) ? region : s.pure_points;
     f[6] = pts <= 8192u ? 1.0 : 0.0;
-    u256 inv1 = n.inv;
-    if (!u256_add_u64(inv1, 1)) return TS_ERR_OVERFLOW;
-    f[7] = (u256_small(inv1) && inv1.w[0] < (uint64_t)LOG2_TABLE) ? log2_int(inv1.w[0]) : fast_log2_u256(inv1);
+    const double inv1 = inv + 1.0;  // exact below 2^53
+    f[7] = inv1 < (double)LOG2_TABLE ? log2_int((uint64_t)inv1) : fast_log2_d(inv1);
     return TS_OK;
   }
 #endif
