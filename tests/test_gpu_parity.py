@@ -401,3 +401,48 @@ def test_exact_sweep_kernels_agree_bitwise(gpu_ctx, v0):
                     os.environ.pop("TS_EXACT_X1", None)
         assert np.all(got[False] > 0)
         assert np.array_equal(bits(got[False]), bits(got[True])), net
+
+
+def test_host_wire_paths_multi_chunk_bitwise(gpu_ctx, v0):
+    """The host-buffer paths score a large batch in chunks whose offsets are
+    absolute (ts_score_states, ts_score_states_packed: the exact leg's rows
+    are indexed from each chunk's first record) or chunk-local
+    (ts_score_states_coded): 300,000 device-generated VGG-16 states - five
+    or more chunks each - equal the device-resident call bit for bit in
+    both legs."""
+    import ctypes
+    import pathlib
+    import torch
+    p = pipeline_from({"text": (pathlib.Path(__file__).resolve().parent.parent
+                                / "assets/pipelines/nets/vgg16.pl").read_text()})
+    inf = ss._info(p)
+    n = 300_000
+    with gpu_ctx.lock:
+        gpu_ctx.set_params(v0)
+        pid = gpu_ctx.pipeline_id(inf.desc)
+        recs = torch.empty(n * inf.T * 16, dtype=torch.uint8, device="cuda")
+        offs = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        nrec = ctypes.c_int64()
+        gpu_ctx.check(gpu_ctx.lib.ts_generate_states_device(gpu_ctx.h, pid, 99, n, recs.data_ptr(),
+                                                            offs.data_ptr(), ctypes.byref(nrec)))
+        h_recs = np.frombuffer(recs[: nrec.value * 16].cpu().numpy().tobytes(), dtype=_lib.DECISION_DTYPE)
+        h_offs = offs.cpu().numpy()
+        depths = np.diff(h_offs).astype(np.uint8)
+        packed = _lib.pack_records(h_recs)
+        codes = ss.action_codes(inf, h_recs, h_offs)
+        assert packed is not None and codes is not None
+        for mode in (MODE_EXACT, MODE_FAST):
+            d = torch.empty(n, dtype=torch.float64, device="cuda")
+            gpu_ctx.check(gpu_ctx.lib.ts_score_states_device(gpu_ctx.h, pid, recs.data_ptr(), offs.data_ptr(), n,
+                                                             nrec.value, mode, d.data_ptr()))
+            want = bits(d.cpu().numpy())
+            for name, call in (
+                    ("records", lambda o: gpu_ctx.lib.ts_score_states(gpu_ctx.h, pid, _lib._p(h_recs),
+                                                                      _lib._p(h_offs), n, mode, _lib._p(o))),
+                    ("packed", lambda o: gpu_ctx.lib.ts_score_states_packed(gpu_ctx.h, pid, _lib._p(packed),
+                                                                            _lib._p(depths), n, mode, _lib._p(o))),
+                    ("coded", lambda o: gpu_ctx.lib.ts_score_states_coded(gpu_ctx.h, pid, _lib._p(codes),
+                                                                          _lib._p(depths), n, mode, _lib._p(o)))):
+                o = np.empty(n)
+                gpu_ctx.check(call(o))
+                assert np.array_equal(bits(o), want), (name, mode)
