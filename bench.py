@@ -998,6 +998,11 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if mode == _lib.MODE_FAST else "f64",
+            "precision": ("tensor-core leg: split-fp16 operands (22-bit), f32 accumulation, MUFU gates; "
+                          "features bit-exact except f13/f15 (big-integer logarithms) to float accuracy "
+                          "before the f32 rounding; V within 1e-4 of the exact fp64 leg (max rel in "
+                          "exact_leg.fast_vs_exact_max_rel), which is bit-identical to the reference"
+                          if mode == _lib.MODE_FAST else "exact fp64 leg, bit-identical to the reference"),
             "data": "synthetic",
             "config": {"workload": "vgg16 synthetic scoring sweep: random partial schedules "
                                    "(SearchRng walk), v0.ckpt", "pipeline": "vgg16", "T": T,
