@@ -158,6 +158,7 @@ struct ts_ctx {
   DevBuf gstat;                 // ts_greedy: distinct children rows (device counter)
   DevBuf ghash;                 // ts_greedy: per-layer children row hashes [T][4096] + counts [T]
   ChildRow child_row{};         // ts_greedy: the fused layer's launch parameters
+  DevBuf beam_ticket;           // ts_beam: the layer kernel's last-block ticket
   DevBuf trc_img;               // TS_TRAIN_TCF: per-step packed weight images
   bool trc_attr_set = false;
   DevBuf beam_rows;             // ts_beam: frontier state rows, double-buffered
@@ -1602,7 +1603,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       cr.hashes = ghash + (size_t)i * kMaxChildren;
       cr.counts = gcount + i;
       cr.status = ctx->status.as<int>();
-      GreedyTail tail;
+      GreedyTail tail{};
       tail.ticket = gticket;
       tail.reset_ticket = 1;
       tail.out = ctx->out.as<double>();
@@ -1913,6 +1914,9 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
   // device state rows of the frontier, double-buffered: [width][T][F]
   const size_t frow = (size_t)T * F;
   TS_CUDA(ctx->beam_rows.reserve(sizeof(double) * frow * 2 * width, ctx->stream));
+  TS_CUDA(ctx->beam_ticket.reserve(sizeof(int), ctx->stream));
+  int* bticket = ctx->beam_ticket.as<int>();
+  TS_CUDA(cudaMemsetAsync(bticket, 0, sizeof(int), ctx->stream));
   TS_CUDA(ctx->h_sel.reserve(sizeof(int) * 2 * width));
   double* cur = ctx->beam_rows.as<double>();
   double* nxt = cur + frow * width;
@@ -1936,6 +1940,13 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
   std::vector<int> parent_of, seg;
   std::vector<std::pair<double, int>> ranked;
   int64_t vis = 0;
+  const bool trace = getenv("TS_BEAM_TRACE") != nullptr;
+  auto now_us = [] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double t_host = 0.0, t_wait = 0.0, t_enum = 0.0;
+  const double t_call = trace ? now_us() : 0.0;
+  double t_mark = t_call;
   for (int i = d0; i < T; ++i) {
     const int s = T - 1 - i;
     const StageDesc& sd = D.st[s];
@@ -1956,6 +1967,12 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
     }
     const int n = (int)cands.size();
     vis += n;
+    if (trace) {
+      const double tn = now_us();
+      t_enum += tn - t_mark;
+      t_host += tn - t_mark;
+      t_mark = tn;
+    }
     // pinned staging: records | parent_of | seg | consumer nests (one H2D)
     const size_t b_rec = sizeof(ts_decision) * n, b_par = sizeof(int) * n, b_seg = sizeof(int) * (W + 1);
     const size_t o_par = b_rec, o_seg = o_par + b_par, o_nest = (o_seg + b_seg + 15) & ~(size_t)15;
@@ -1989,21 +2006,45 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
     if (xs_bytes > 40 * 1024)
       TS_CUDA(cudaFuncSetAttribute(k_children_exact_mw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)xs_bytes));
+    // the last CTA writes every child's V and the device status into mapped
+    // host memory and then a sequence number, which the host polls (no
+    // copies, no stream sync per layer)
+    TS_CUDA(ctx->h_out.reserve(sizeof(double) * (n + 4)));
+    double* hv = ctx->h_out.as<double>();
+    volatile double* ho = hv + n;  // {-, -, status, seq}
+    const double seq = (double)++ctx->greedy_seq;
+    ho[3] = 0.0;
+    GreedyTail tail{};
+    tail.ticket = bticket;
+    tail.reset_ticket = 1;
+    tail.status = ctx->status.as<int>();
+    tail.target_scale = ctx->target_scale;
+    tail.host_v = hv;
+    tail.host_out = ho;
+    tail.seq = seq;
     k_children_exact_mw<<<n, 128, xs_bytes, ctx->stream>>>(lstm_weights(ctx), P->pre_exact.as<double>(), T, s,
                                                            ctx->rows.as<double>(), ctx->reps.as<int>(), n, cur,
-                                                           raw, nullptr, GreedyTail{}, d_par);
+                                                           raw, nullptr, tail, d_par);
     TS_LAUNCHED();
-    double* dv = raw + n;
-    k_children_v<<<(n + 127) / 128, 128, 0, ctx->stream>>>(raw, ctx->reps.as<int>(), n, ctx->target_scale, dv);
-    TS_LAUNCHED();
-    TS_CUDA(ctx->h_out.reserve(sizeof(double) * n + sizeof(int)));
-    double* hv = ctx->h_out.as<double>();
-    TS_CUDA(cudaMemcpyAsync(hv, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    int* hst = reinterpret_cast<int*>(hv + n);
-    TS_CUDA(cudaMemcpyAsync(hst, ctx->status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    TS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (*hst) {
-      const int st = *hst;
+    if (trace) {
+      const double tn = now_us();
+      t_host += tn - t_mark;
+      t_mark = tn;
+    }
+    for (uint32_t spin = 1; ho[3] != seq; ++spin) {
+      if ((spin & 4095u) == 0) {
+        const cudaError_t q = cudaStreamQuery(ctx->stream);
+        if (q != cudaSuccess && q != cudaErrorNotReady) TS_CUDA(q);
+        if (q == cudaSuccess && ho[3] != seq) return fail(ctx, TS_ERR_CUDA, "beam layer wrote no result");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);  // V and status were written before seq
+    if (trace) {
+      const double tn = now_us();
+      t_wait += tn - t_mark;
+      t_mark = tn;
+    }
+    if (const int st = (int)ho[2]) {
       cudaMemset(ctx->status.p, 0, sizeof(int));
       return fail(ctx, st, std::string("device: ") + status_name(st));
     }
@@ -2046,6 +2087,10 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
   memcpy(out_decisions, frontier[0].decs.data(), sizeof(ts_decision) * T);
   if (visited) *visited = vis;
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (trace)
+    fprintf(stderr, "ts_beam: T %d, width %d, visited %lld: host %.0f us (of which rank + frontier + enumerate "
+            "%.0f us), waiting %.0f us, total %.0f us\n", T, width, (long long)vis, t_host, t_enum, t_wait,
+            now_us() - t_call);
   return TS_OK;
 }
 
