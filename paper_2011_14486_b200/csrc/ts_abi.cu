@@ -3,10 +3,12 @@
 //
 // The greedy driver (ts_greedy) is the fused replacement of
 // search.greedy_schedule (search.py:90-112): per layer it enumerates the
-// candidates on the host (the integer nest math is tiny), then one stream
-// of kernels featurizes the children, dedups identical rows, runs the exact
-// LSTM from the shared prefix and reduces the argmin; only the winner's
-// index comes back.  Only the winner is "applied" (hard part 7).
+// candidates on the host (the integer nest math is tiny) and launches ONE
+// kernel (hidden size 32) whose CTAs featurize their child's new row and run
+// the exact LSTM from the shared prefix, the last CTA reducing the argmin
+// and installing the winner's row; only {v, index, status} comes back,
+// through mapped host memory.  Only the winner is "applied" (SURVEY.md 7,
+// hard part 7).
 #include <cuda_runtime.h>
 #if defined(__SSE2__)
 #include <emmintrin.h>
