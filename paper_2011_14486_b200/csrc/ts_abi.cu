@@ -825,25 +825,33 @@ static int score_device(ts_ctx* ctx, PipelineSlot* P, const ts_decision* d_recor
           tc::k_depth_scatter<<<(unsigned)((n_states + per_block - 1) / per_block), tc::SCATTER_THREADS,
                                 sizeof(int) * 2 * (T + 1), ctx->stream>>>(d_offsets, n_states, T, cursor, perm);
           TS_LAUNCHED();
-          const bool four = getenv("TS_EXACT_X4") != nullptr;
-          const size_t smn = four ? exact32xn_smem<4>(256) : exact32xn_smem<2>(256);
+          // states per warp (TS_EXACT_NS: 2, 3 or 4; 2 measured best)
+          int ns = 2;
+          if (const char* e = getenv("TS_EXACT_NS")) ns = std::min(4, std::max(2, atoi(e)));
           if (!ctx->exact2_attr_set) {
             TS_CUDA(cudaFuncSetAttribute(k_score_exact32xn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)exact32xn_smem<2>(256)));
+            TS_CUDA(cudaFuncSetAttribute(k_score_exact32xn<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)exact32xn_smem<3>(256)));
             TS_CUDA(cudaFuncSetAttribute(k_score_exact32xn<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)exact32xn_smem<4>(256)));
             ctx->exact2_attr_set = true;
           }
-          const int ns = four ? 4 : 2;
           const int64_t warps = (n_states + ns - 1) / ns;
-          if (four)
-            k_score_exact32xn<4><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
-                lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
-                n_states, ctx->target_scale, d_out, rec_base);
+          const unsigned grid = (unsigned)((warps + 7) / 8);
+          const LstmW W = lstm_weights(ctx);
+          if (ns == 4)
+            k_score_exact32xn<4><<<grid, 256, exact32xn_smem<4>(256), ctx->stream>>>(
+                W, P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm, n_states,
+                ctx->target_scale, d_out, rec_base);
+          else if (ns == 3)
+            k_score_exact32xn<3><<<grid, 256, exact32xn_smem<3>(256), ctx->stream>>>(
+                W, P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm, n_states,
+                ctx->target_scale, d_out, rec_base);
           else
-            k_score_exact32xn<2><<<(unsigned)((warps + 7) / 8), 256, smn, ctx->stream>>>(
-                lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm,
-                n_states, ctx->target_scale, d_out, rec_base);
+            k_score_exact32xn<2><<<grid, 256, exact32xn_smem<2>(256), ctx->stream>>>(
+                W, P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), perm, n_states,
+                ctx->target_scale, d_out, rec_base);
         } else {
           k_score_exact32<<<(unsigned)((threads + 511) / 512), 512, sizeof(ExactSmem), ctx->stream>>>(
               lstm_weights(ctx), P->pre_exact.as<double>(), T, d_offsets, ctx->rows.as<double>(), n_states,
