@@ -249,37 +249,39 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
   constexpr float S1 = 8.673617379884035e-19f;  // 2^-60
   constexpr float S2 = 9.094947017729282e-13f;  // 2^-40
   constexpr float C2 = -2.0f * LOG2E;
+  // The two units of a pair go through the sm_100 paired fp32 pipe
+  // (FFMA2 / FMUL2: two IEEE fmas / products per instruction, each lane the
+  // same rounding as FFMA / FMUL, so the values are the scalar code's bit for
+  // bit) - the epilogue is issue-bound next to its MUFU work.
+  const float2 s1 = make_float2(S1, S1), ns1 = make_float2(-S1, -S1);
+  const float2 s2 = make_float2(S2, S2), ns2 = make_float2(-S2, -S2);
 #pragma unroll
   for (int u = 0; u < 8; u += 2) {
-    float tig[2], num[2], d1[2], eo[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int uu = u + q, j = g8 * 8 + uu;
-      const float ei = ex2_sel(clamp40(ui[uu]), 0), ef = ex2_sel(clamp40(uf[uu]), 1);
-      const float eg = ex2_sel(clamp40(vg[uu]), 2);
-      eo[q] = ex2_sel(clamp40(uo[uu]), 3);
-      // products by (1 + e) as fused a + a e: t_f is never formed
-      const float ti = fmaf(ei, S1, S1);                 // 2^-60 t_i
-      tig[q] = fmaf(ti, eg, ti);                         // 2^-60 t_i t_g
-      const float gm = fmaf(-eg, S1, S1);                // 2^-60 (1 - e_g)
-      num[q] = fmaf(c[j], tig[q], fmaf(gm, ef, gm));     // 2^-60 (c t_i t_g + (1 - e_g) t_f)
-      d1[q] = fmaf(tig[q], ef, tig[q]);                  // 2^-60 t_f t_i t_g
-    }
-    const float r1 = rcp(d1[0] * d1[1]);
-    c[g8 * 8 + u] = num[0] * (d1[1] * r1);
-    c[g8 * 8 + u + 1] = num[1] * (d1[0] * r1);
-    float ec[2], d2[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      ec[q] = ex2_sel(clamp40(C2 * c[g8 * 8 + u + q]), 4);
-      const float to = fmaf(eo[q], S2, S2);             // 2^-40 (1 + e_o)
-      d2[q] = fmaf(to, ec[q], to);                       // 2^-40 (1 + e_o)(1 + e_c)
-    }
-    const float r2 = rcp(d2[0] * d2[1]);
-    h8[u] = fmaf(-ec[0], S2, S2) * (d2[1] * r2);
-    h8[u + 1] = fmaf(-ec[1], S2, S2) * (d2[0] * r2);
-    acc = fmaf(h8[u], wout[g8 * 8 + u], acc);
-    acc = fmaf(h8[u + 1], wout[g8 * 8 + u + 1], acc);
+    const int j = g8 * 8 + u;
+    const float2 ei = make_float2(ex2_sel(clamp40(ui[u]), 0), ex2_sel(clamp40(ui[u + 1]), 0));
+    const float2 ef = make_float2(ex2_sel(clamp40(uf[u]), 1), ex2_sel(clamp40(uf[u + 1]), 1));
+    const float2 eg = make_float2(ex2_sel(clamp40(vg[u]), 2), ex2_sel(clamp40(vg[u + 1]), 2));
+    const float2 eo = make_float2(ex2_sel(clamp40(uo[u]), 3), ex2_sel(clamp40(uo[u + 1]), 3));
+    // products by (1 + e) as fused a + a e: t_f is never formed
+    const float2 ti = __ffma2_rn(ei, s1, s1);                                  // 2^-60 t_i
+    const float2 tig = __ffma2_rn(ti, eg, ti);                                 // 2^-60 t_i t_g
+    const float2 gm = __ffma2_rn(eg, ns1, s1);                                 // 2^-60 (1 - e_g)
+    const float2 num = __ffma2_rn(make_float2(c[j], c[j + 1]), tig, __ffma2_rn(gm, ef, gm));
+    const float2 d1 = __ffma2_rn(tig, ef, tig);                                // 2^-60 t_f t_i t_g
+    const float r1 = rcp(d1.x * d1.y);
+    const float2 cn = __fmul2_rn(num, __fmul2_rn(make_float2(d1.y, d1.x), make_float2(r1, r1)));
+    c[j] = cn.x;
+    c[j + 1] = cn.y;
+    const float2 cc = __fmul2_rn(make_float2(C2, C2), cn);
+    const float2 ec = make_float2(ex2_sel(clamp40(cc.x), 4), ex2_sel(clamp40(cc.y), 4));
+    const float2 to = __ffma2_rn(eo, s2, s2);                                  // 2^-40 (1 + e_o)
+    const float2 d2 = __ffma2_rn(to, ec, to);                                  // 2^-40 (1 + e_o)(1 + e_c)
+    const float r2 = rcp(d2.x * d2.y);
+    const float2 hh = __fmul2_rn(__ffma2_rn(ec, ns2, s2), __fmul2_rn(make_float2(d2.y, d2.x), make_float2(r2, r2)));
+    h8[u] = hh.x;
+    h8[u + 1] = hh.y;
+    acc = fmaf(hh.x, wout[j], acc);
+    acc = fmaf(hh.y, wout[j + 1], acc);
   }
 }
 
