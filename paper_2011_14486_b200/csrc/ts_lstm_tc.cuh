@@ -154,11 +154,36 @@ __device__ __forceinline__ float ex2_fma(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
+// ex2_fma for a unit pair on the paired fp32 pipe (FADD2 / FFMA2), the
+// argument clamped to [-40, 40] (below -40, 1 + 2^x is 1 in fp32 either way)
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -40.0f);
+  x.y = fmaxf(x.y, -40.0f);
+  const float2 sh = make_float2(12582912.0f, 12582912.0f), nsh = make_float2(-12582912.0f, -12582912.0f);
+  const float2 t = __fadd2_rn(x, sh);
+  const float2 f = __fadd2_rn(x, make_float2(-__fadd_rn(t.x, -12582912.0f), -__fadd_rn(t.y, -12582912.0f)));
+  (void)nsh;
+  float2 p = __ffma2_rn(make_float2(0.0013276466634124517f, 0.0013276466634124517f), f,
+                        make_float2(0.009675540961325169f, 0.009675540961325169f));
+  p = __ffma2_rn(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
+  p = __ffma2_rn(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + ((__float_as_int(t.x) - 0x4B400000) << 23)),
+                     __int_as_float(__float_as_int(p.y) + ((__float_as_int(t.y) - 0x4B400000) << 23)));
+}
+
 #ifndef TS_FMA_EXP
 #define TS_FMA_EXP 0  // how many of the 5 per-unit exponentials use ex2_fma
 #endif
 __device__ __forceinline__ float ex2_sel(float x, int slot) {
   return slot < TS_FMA_EXP ? ex2_fma(x) : ex2(x);
+}
+// a unit pair's exponential of slot `slot` (the arguments already clamped
+// above at 40)
+__device__ __forceinline__ float2 ex2_pair(float a, float b, int slot) {
+  if (slot < TS_FMA_EXP) return ex2_fma2(make_float2(a, b));
+  return make_float2(ex2(a), ex2(b));
 }
 
 // Stores 16-byte chunk `kc` of row `r` in the canonical no-swizzle layout.
@@ -258,10 +283,10 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
 #pragma unroll
   for (int u = 0; u < 8; u += 2) {
     const int j = g8 * 8 + u;
-    const float2 ei = make_float2(ex2_sel(clamp40(ui[u]), 0), ex2_sel(clamp40(ui[u + 1]), 0));
-    const float2 ef = make_float2(ex2_sel(clamp40(uf[u]), 1), ex2_sel(clamp40(uf[u + 1]), 1));
-    const float2 eg = make_float2(ex2_sel(clamp40(vg[u]), 2), ex2_sel(clamp40(vg[u + 1]), 2));
-    const float2 eo = make_float2(ex2_sel(clamp40(uo[u]), 3), ex2_sel(clamp40(uo[u + 1]), 3));
+    const float2 ei = ex2_pair(clamp40(ui[u]), clamp40(ui[u + 1]), 0);
+    const float2 ef = ex2_pair(clamp40(uf[u]), clamp40(uf[u + 1]), 1);
+    const float2 eg = ex2_pair(clamp40(vg[u]), clamp40(vg[u + 1]), 2);
+    const float2 eo = ex2_pair(clamp40(uo[u]), clamp40(uo[u + 1]), 3);
     // products by (1 + e) as fused a + a e: t_f is never formed
     const float2 ti = __ffma2_rn(ei, s1, s1);                                  // 2^-60 t_i
     const float2 tig = __ffma2_rn(ti, eg, ti);                                 // 2^-60 t_i t_g
@@ -273,7 +298,7 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
     c[j] = cn.x;
     c[j + 1] = cn.y;
     const float2 cc = __fmul2_rn(make_float2(C2, C2), cn);
-    const float2 ec = make_float2(ex2_sel(clamp40(cc.x), 4), ex2_sel(clamp40(cc.y), 4));
+    const float2 ec = ex2_pair(clamp40(cc.x), clamp40(cc.y), 4);
     const float2 to = __ffma2_rn(eo, s2, s2);                                  // 2^-40 (1 + e_o)
     const float2 d2 = __ffma2_rn(to, ec, to);                                  // 2^-40 (1 + e_o)(1 + e_c)
     const float r2 = rcp(d2.x * d2.y);
