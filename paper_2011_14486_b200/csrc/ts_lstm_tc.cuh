@@ -173,6 +173,9 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + ((__float_as_int(t.y) - 0x4B400000) << 23)));
 }
 
+#ifndef TS_QUAD_RCP
+#define TS_QUAD_RCP 0  // 1: the output gate's reciprocal shared by four units (cell_group; measured 1%, off)
+#endif
 #ifndef TS_FMA_EXP
 #define TS_FMA_EXP 0  // how many of the 5 per-unit exponentials use ex2_fma
 #endif
@@ -279,6 +282,53 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
   // same rounding as FFMA / FMUL, so the values are the scalar code's bit for
   // bit) - the epilogue is issue-bound next to its MUFU work.
   const float2 s1 = make_float2(S1, S1), ns1 = make_float2(-S1, -S1);
+#if TS_QUAD_RCP
+  // the output gate's reciprocal is shared by four units (one rcp per
+  // quad): 1 + e_o and 1 + e_c clamped at 2^30 and scaled by 2^-30 keep the
+  // product of four denominators inside [2^-120, 2^120]; sigma(o) and
+  // tanh(c) then saturate at 2^-30 instead of 2^-40 (|error| < 1e-9)
+  constexpr float S2Q = 9.313225746154785e-10f;  // 2^-30
+  const float2 s2 = make_float2(S2Q, S2Q), ns2 = make_float2(-S2Q, -S2Q);
+#pragma unroll
+  for (int u4 = 0; u4 < 8; u4 += 4) {
+    float2 ecq[2], d2q[2];
+#pragma unroll
+    for (int hq = 0; hq < 2; ++hq) {
+      const int u = u4 + 2 * hq, j = g8 * 8 + u;
+      const float2 ei = ex2_pair(clamp40(ui[u]), clamp40(ui[u + 1]), 0);
+      const float2 ef = ex2_pair(clamp40(uf[u]), clamp40(uf[u + 1]), 1);
+      const float2 eg = ex2_pair(clamp40(vg[u]), clamp40(vg[u + 1]), 2);
+      const float2 eo = ex2_pair(fminf(uo[u], 30.0f), fminf(uo[u + 1], 30.0f), 3);
+      const float2 ti = __ffma2_rn(ei, s1, s1);                                  // 2^-60 t_i
+      const float2 tig = __ffma2_rn(ti, eg, ti);                                 // 2^-60 t_i t_g
+      const float2 gm = __ffma2_rn(eg, ns1, s1);                                 // 2^-60 (1 - e_g)
+      const float2 num = __ffma2_rn(make_float2(c[j], c[j + 1]), tig, __ffma2_rn(gm, ef, gm));
+      const float2 d1 = __ffma2_rn(tig, ef, tig);                                // 2^-60 t_f t_i t_g
+      const float r1 = rcp(d1.x * d1.y);
+      const float2 cn = __fmul2_rn(num, __fmul2_rn(make_float2(d1.y, d1.x), make_float2(r1, r1)));
+      c[j] = cn.x;
+      c[j + 1] = cn.y;
+      const float2 cc = __fmul2_rn(make_float2(C2, C2), cn);
+      ecq[hq] = ex2_pair(fminf(cc.x, 30.0f), fminf(cc.y, 30.0f), 4);
+      const float2 to = __ffma2_rn(eo, s2, s2);                                  // 2^-30 (1 + e_o)
+      d2q[hq] = __ffma2_rn(to, ecq[hq], to);                                     // 2^-30 (1 + e_o)(1 + e_c)
+    }
+    const float p0 = d2q[0].x * d2q[0].y, p1 = d2q[1].x * d2q[1].y;
+    const float rq = rcp(p0 * p1);
+    const float r20 = p1 * rq, r21 = p0 * rq;  // 1 / p0, 1 / p1
+#pragma unroll
+    for (int hq = 0; hq < 2; ++hq) {
+      const int u = u4 + 2 * hq, j = g8 * 8 + u;
+      const float r2 = hq ? r21 : r20;
+      const float2 hh = __fmul2_rn(__ffma2_rn(ecq[hq], ns2, s2),
+                                   __fmul2_rn(make_float2(d2q[hq].y, d2q[hq].x), make_float2(r2, r2)));
+      h8[u] = hh.x;
+      h8[u + 1] = hh.y;
+      acc = fmaf(hh.x, wout[j], acc);
+      acc = fmaf(hh.y, wout[j + 1], acc);
+    }
+  }
+#else
   const float2 s2 = make_float2(S2, S2), ns2 = make_float2(-S2, -S2);
 #pragma unroll
   for (int u = 0; u < 8; u += 2) {
@@ -308,6 +358,7 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
     acc = fmaf(hh.x, wout[j], acc);
     acc = fmaf(hh.y, wout[j + 1], acc);
   }
+#endif
 }
 
 // kNWG warpgroups (tiles in flight) per CTA: 4 for large batches; 1 or 2
