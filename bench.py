@@ -803,7 +803,7 @@ def main():
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     # ncu --set full captures (profiles/r02_ncu.md): DRAM bytes per state of each
     # kernel at 12.5M states (this bench's default launch), scaled to this launch
-    traffic_per_state = {"featurize": (6.280675e9 + 7.027746e9) / 12.5e6,
+    traffic_per_state = {"featurize": (6.285197e9 + 7.072871e9) / 12.5e6,
                          "lstm_fast": (8.762989e9 + 0.379514e9) / 12.5e6}
     row_bytes = 32 if mode == _lib.MODE_FAST else ROW_BYTES  # FAST rows: 8 acquired f32
     if dom == "featurize":
@@ -857,14 +857,14 @@ def main():
     if "featurize" in avg and mode == _lib.MODE_FAST:
         # the featurizer's binding resource is instruction issue (integer
         # walk): warp instructions per scheduled row from the ncu capture
-        # (6.4274e9 warp instructions for 12.5M states = 218.7M rows,
+        # (6.3449e9 warp instructions for 12.5M states = 218.7M rows,
         # profiles/r02_ncu.md), against 4 warp instructions / clk / SM
         mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965
         issue_peak = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * mhz * 1e6
-        issued = 6.427419e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
+        issued = 6.344893e9 / 218.7e6 * timesteps / (avg["featurize"] / 1e3)
         roof["k_featurize_rows_issue"] = {"bound": "issue", "achieved": issued / 1e12, "peak": issue_peak / 1e12,
                                           "unit": "T warp-instr/s", "frac": issued / issue_peak,
-                                          "algorithmic": "29.4 warp instructions per scheduled row (ncu)",
+                                          "algorithmic": "29.0 warp instructions per scheduled row (ncu)",
                                           "instructions_source": "constant from one ncu --set full "
                                                                  "capture (profiles/r02_ncu.md), not "
                                                                  "measured in this run"}
