@@ -86,3 +86,31 @@ def test_random_pipeline_device_parity(v0_path):
         s, visited = greedy_schedule_gpu(p, params)
         gw, gv = O.greedy(P, oparams)
         assert [d.render() for d in s.decisions] == [a.render() for a in gw] and visited == gv, seed
+
+
+@pytest.mark.gpu
+def test_random_pipeline_beam_parity(v0_path):
+    """The fused device beam (ts_beam) against the oracle's beam_search
+    restatement on the random pipelines (widths 2 and 4, from the empty
+    prefix and from a two-decision prefix): identical completions, V bit for
+    bit (the exact leg ranks them)."""
+    from paper_2011_14486_b200.search import beam_search_gpu
+    from paper_2011_14486_b200.value_model import load
+    params = load(v0_path)
+    oparams = O.load_checkpoint(v0_path)
+    checked = 0
+    for seed, text in enumerate(_texts()):
+        p = pi.parse_pipeline(text)
+        P = O.Pipe(p)
+        if len(P.topo) > 12:  # the oracle beam is pure Python
+            continue
+        for width, plen in ((2, 0), (4, 2)):
+            prefix = _walks(P, 1, 7 * seed + width)[0][:plen] if plen else []
+            if len(prefix) >= len(P.topo):
+                continue
+            want = O.beam(P, oparams, prefix, width)
+            s, v = beam_search_gpu(ss.state_from_decisions(p, prefix), params, width, return_value=True)
+            assert [d.render() for d in s.decisions] == [a.render() for a in want], (seed, width, plen)
+            assert np.array_equal(bits(np.array([v])), bits(O.values(oparams, P, [want]))), (seed, width)
+            checked += 1
+    assert checked >= 20
