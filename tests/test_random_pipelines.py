@@ -114,3 +114,23 @@ def test_random_pipeline_beam_parity(v0_path):
             assert np.array_equal(bits(np.array([v])), bits(O.values(oparams, P, [want]))), (seed, width)
             checked += 1
     assert checked >= 20
+
+
+@pytest.mark.gpu
+def test_random_pipeline_noisy_greedy_parity(v0_path):
+    """The fused device greedy with noise (epsilon 0.25, the learner's
+    rollouts) against the oracle's greedy with its SplitMix stream on every
+    random pipeline: identical schedules, visited counts and final rng
+    state."""
+    from paper_2011_14486_b200.search import NoiseConfig, SearchRng, greedy_schedule_gpu
+    from paper_2011_14486_b200.value_model import load
+    params = load(v0_path)
+    oparams = O.load_checkpoint(v0_path)
+    for seed, text in enumerate(_texts()):
+        p = pi.parse_pipeline(text)
+        P = O.Pipe(p)
+        rng, orng = SearchRng(1000 + seed), O.SplitMix(1000 + seed)
+        s, visited = greedy_schedule_gpu(p, params, NoiseConfig(0.25), rng)
+        want, ov = O.greedy(P, oparams, 0.25, orng)
+        assert [d.render() for d in s.decisions] == [a.render() for a in want], seed
+        assert visited == ov and rng.state == orng.state, seed
