@@ -134,3 +134,26 @@ def test_random_pipeline_noisy_greedy_parity(v0_path):
         want, ov = O.greedy(P, oparams, 0.25, orng)
         assert [d.render() for d in s.decisions] == [a.render() for a in want], seed
         assert visited == ov and rng.state == orng.state, seed
+
+
+@pytest.mark.gpu
+def test_random_pipeline_score_children_parity(v0_path):
+    """ts_score_children (one layer step for any parent: the parent's rows
+    once, each child's new row, dedup, the exact suffix LSTM) against the
+    oracle's V of the materialized children, bit for bit, on two random
+    prefixes of every random pipeline."""
+    from paper_2011_14486_b200.search import score_children
+    from paper_2011_14486_b200.value_model import load
+    params = load(v0_path)
+    oparams = O.load_checkpoint(v0_path)
+    for seed, text in enumerate(_texts()):
+        p = pi.parse_pipeline(text)
+        P = O.Pipe(p)
+        for decs in _walks(P, 2, 31 * seed + 5):
+            if len(decs) >= len(P.topo):
+                decs = decs[:-1]
+            s = ss.state_from_decisions(p, decs)
+            acts = ss.candidate_actions(s)
+            got = score_children(params, s, acts)
+            want = O.values(oparams, P, [list(decs) + [O.as_act(a)] for a in acts])
+            assert np.array_equal(bits(np.asarray(got)), bits(want)), seed
