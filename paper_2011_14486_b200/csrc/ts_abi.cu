@@ -53,7 +53,17 @@ struct DevBuf {
     bytes = 0;
     cudaError_t e = cudaMalloc(&p, n);
     if (e == cudaSuccess) bytes = n;
+    // TS_POISON (tests): new allocations start as all-ones bytes (NaN as
+    // doubles, -1 as integers), so a read of never-written memory shows up
+    if (e == cudaSuccess && poison()) {
+      e = cudaMemset(p, 0xFF, n);
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
     return e;
+  }
+  static bool poison() {
+    static const bool on = getenv("TS_POISON") != nullptr;
+    return on;
   }
   // Growth of a buffer that kernels queued on `user` may still read: wait
   // for that stream before the old allocation is released (explicitly, not
@@ -572,6 +582,15 @@ void* ts_stream(ts_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int64_t ts_launch_count(ts_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
+// Clear the device status word after a reported failure: drain the stream
+// first (kernels of the failed call may still be running and write it), then
+// clear it in stream order.
+static void reset_status(ts_ctx* ctx) {
+  cudaStreamSynchronize(ctx->stream);
+  cudaMemsetAsync(ctx->status.p, 0, sizeof(int), ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+}
+
 int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* pipeline_id) {
   if (!ctx || !desc || !pipeline_id) return TS_ERR_ARG;
   if (n_words < DESC_HEADER || desc[0] != 0x54534231 /* "TSB1" */)
@@ -633,7 +652,8 @@ int ts_pipeline_upload(ts_ctx* ctx, const int64_t* desc, int64_t n_words, int* p
   if (ctx->device >= 0) {
     TS_CUDA(cudaSetDevice(ctx->device));
     TS_CUDA(slot->d.reserve(sizeof(PipelineDesc)));
-    TS_CUDA(cudaMemcpy(slot->d.p, &P, sizeof(PipelineDesc), cudaMemcpyHostToDevice));
+    TS_CUDA(cudaMemcpyAsync(slot->d.p, &P, sizeof(PipelineDesc), cudaMemcpyHostToDevice, ctx->stream));
+    TS_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   ctx->pipes.push_back(std::move(slot));
   *pipeline_id = (int)ctx->pipes.size() - 1;
@@ -655,12 +675,12 @@ int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh
   TS_CUDA(ctx->w.reserve(sizeof(double) * hidden));
   TS_CUDA(ctx->mean.reserve(sizeof(double) * F));
   TS_CUDA(ctx->stdv.reserve(sizeof(double) * F));
-  TS_CUDA(cudaMemcpy(ctx->Wx.p, Wx, sizeof(double) * F * G, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->Wh.p, Wh, sizeof(double) * hidden * G, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->b.p, b, sizeof(double) * G, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->w.p, w, sizeof(double) * hidden, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->mean.p, norm_mean, sizeof(double) * F, cudaMemcpyHostToDevice));
-  TS_CUDA(cudaMemcpy(ctx->stdv.p, norm_std, sizeof(double) * F, cudaMemcpyHostToDevice));
+  TS_CUDA(cudaMemcpyAsync(ctx->Wx.p, Wx, sizeof(double) * F * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->Wh.p, Wh, sizeof(double) * hidden * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->b.p, b, sizeof(double) * G, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->w.p, w, sizeof(double) * hidden, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->mean.p, norm_mean, sizeof(double) * F, cudaMemcpyHostToDevice, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->stdv.p, norm_std, sizeof(double) * F, cudaMemcpyHostToDevice, ctx->stream));
   ctx->hidden = hidden;
   ctx->b_out = b_out;
   ctx->target_scale = target_scale;
@@ -670,8 +690,9 @@ int ts_params_upload(ts_ctx* ctx, int hidden, const double* Wx, const double* Wh
     std::vector<uint8_t> img(tc::TILE_BYTES + 4 * 32);
     tc::pack_weights(Wx, Wh, b, w, img.data());
     TS_CUDA(ctx->fast_w.reserve(img.size()));
-    TS_CUDA(cudaMemcpy(ctx->fast_w.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+    TS_CUDA(cudaMemcpyAsync(ctx->fast_w.p, img.data(), img.size(), cudaMemcpyHostToDevice, ctx->stream));
   }
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   return TS_OK;
 }
 
@@ -1653,7 +1674,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
       std::atomic_thread_fence(std::memory_order_acquire);
       const int st = (int)ho[2];
       if (st) {
-        cudaMemset(ctx->status.p, 0, sizeof(int));
+        reset_status(ctx);
         return fail(ctx, st, std::string("device: ") + status_name(st));
       }
       const int best = (int)ho[1];
@@ -1713,7 +1734,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
     if (trace) t_wait += now_us() - tw0;
     const int st = *hst;
     if (st) {
-      cudaMemset(ctx->status.p, 0, sizeof(int));
+      reset_status(ctx);
       return fail(ctx, st, std::string("device: ") + status_name(st));
     }
     const int best = (int)ho[1];
@@ -1862,7 +1883,7 @@ int ts_score_children(ts_ctx* ctx, int pipeline_id, const ts_decision* parent, i
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (*hst) {
     const int st = *hst;
-    cudaMemset(ctx->status.p, 0, sizeof(int));
+    reset_status(ctx);
     return fail(ctx, st, std::string("device: ") + status_name(st));
   }
   if (out_v) memcpy(out_v, ho + 2, sizeof(double) * n);
@@ -2055,7 +2076,7 @@ int ts_beam(ts_ctx* ctx, int pipeline_id, const ts_decision* prefix, int64_t n_p
       t_mark = tn;
     }
     if (const int st = (int)ho[2]) {
-      cudaMemset(ctx->status.p, 0, sizeof(int));
+      reset_status(ctx);
       return fail(ctx, st, std::string("device: ") + status_name(st));
     }
     // sorted(range(len(children)), key=(v, i))[:width]
@@ -2247,7 +2268,8 @@ int ts_train_load(ts_ctx* ctx, const double* rows, int64_t n_rows, const double*
   TS_CUDA(cudaStreamSynchronize(ctx->stream));
   const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   std::vector<int32_t> hT(N);
-  TS_CUDA(cudaMemcpy(hT.data(), Tlen, sizeof(int32_t) * N, device_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  TS_CUDA(cudaMemcpyAsync(hT.data(), Tlen, sizeof(int32_t) * N, device_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, ctx->stream));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   int Tmax = 1;
   for (int64_t i = 0; i < N; ++i) Tmax = std::max(Tmax, (int)hT[i]);
   ctx->tr_H = hidden;
@@ -2260,13 +2282,13 @@ int ts_train_load(ts_ctx* ctx, const double* rows, int64_t n_rows, const double*
   double* dinit = drows + n_rows * F;
   int64_t* drb = ctx->tr_T.as<int64_t>();
   int32_t* dib = reinterpret_cast<int32_t*>(drb + N);
-  TS_CUDA(cudaMemcpy(drows, rows, sizeof(double) * n_rows * F, kind));
-  if (n_init) TS_CUDA(cudaMemcpy(dinit, init, sizeof(double) * n_init * F, kind));
-  TS_CUDA(cudaMemcpy(drb, row_base, sizeof(int64_t) * N, kind));
-  TS_CUDA(cudaMemcpy(dib, init_base, sizeof(int32_t) * N, kind));
-  TS_CUDA(cudaMemcpy(dib + N, Tlen, sizeof(int32_t) * N, kind));
-  TS_CUDA(cudaMemcpy(dib + 2 * N, depth, sizeof(int32_t) * N, kind));
-  TS_CUDA(cudaMemcpy(ctx->tr_logt.p, logt, sizeof(double) * N, kind));
+  TS_CUDA(cudaMemcpyAsync(drows, rows, sizeof(double) * n_rows * F, kind, ctx->stream));
+  if (n_init) TS_CUDA(cudaMemcpyAsync(dinit, init, sizeof(double) * n_init * F, kind, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(drb, row_base, sizeof(int64_t) * N, kind, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dib, init_base, sizeof(int32_t) * N, kind, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dib + N, Tlen, sizeof(int32_t) * N, kind, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(dib + 2 * N, depth, sizeof(int32_t) * N, kind, ctx->stream));
+  TS_CUDA(cudaMemcpyAsync(ctx->tr_logt.p, logt, sizeof(double) * N, kind, ctx->stream));
   ctx->tr_data.rows = drows;
   ctx->tr_data.init = dinit;
   ctx->tr_data.row_base = drb;
@@ -2278,6 +2300,7 @@ int ts_train_load(ts_ctx* ctx, const double* rows, int64_t n_rows, const double*
   TS_CUDA(ctx->tr_P.reserve(sizeof(double) * L.n));
   TS_CUDA(ctx->tr_grad.reserve(sizeof(double) * L.n));
   TS_CUDA(ctx->tr_norm.reserve(sizeof(double)));
+  TS_CUDA(cudaStreamSynchronize(ctx->stream));
   return TS_OK;
 }
 
