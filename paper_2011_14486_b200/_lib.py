@@ -70,7 +70,9 @@ _lib_lock = threading.Lock()
 
 
 def _p(arr):
-    return ctypes.c_void_p(arr.ctypes.data) if arr is not None else None
+    # data_as: the pointer object keeps the array alive for the call, so a
+    # temporary (`_p(x.copy())`) cannot be freed before the C side reads it
+    return arr.ctypes.data_as(ctypes.c_void_p) if arr is not None else None
 
 
 def load_library():

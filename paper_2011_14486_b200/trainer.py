@@ -84,10 +84,11 @@ class DeviceGradients:
         rows = np.concatenate([X[i, : T[i]][::-1] for i in range(len(T))])
         rows = np.ascontiguousarray(rows)
         zeros = np.zeros(len(T), dtype=np.int32)
+        depth = T.copy()  # every row scheduled
+        logt = np.ascontiguousarray(logt, dtype=np.float64)
         ctx.check(ctx.lib.ts_train_load(
             ctx.h, _lib._p(rows), rows.shape[0], None, 0, _lib._p(base), _lib._p(zeros),
-            _lib._p(T), _lib._p(T.copy()), _lib._p(np.ascontiguousarray(logt, dtype=np.float64)),
-            len(T), hidden, 0))
+            _lib._p(T), _lib._p(depth), _lib._p(logt), len(T), hidden, 0))
         self.set_mode(mode)
 
     def set_mode(self, mode):
