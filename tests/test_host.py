@@ -32,6 +32,19 @@ def test_library_exports_every_declared_symbol():
     assert lib.ts_abi_version() == 1
 
 
+def test_pointer_keeps_temporary_alive():
+    """_lib._p(temporary) must keep the array alive until the C call: a bare
+    address let numpy free `T.copy()` before ts_train_load read it (a
+    training run on corrupted depths, seen as a rare flaky parity failure)."""
+    import gc
+    p = _lib._p(np.arange(1000, dtype=np.int32).copy())
+    gc.collect()
+    junk = [np.full(1000, -7, dtype=np.int32) for _ in range(64)]  # reuse freed blocks
+    view = ctypes.cast(p, ctypes.POINTER(ctypes.c_int32))
+    assert [view[i] for i in (0, 1, 500, 999)] == [0, 1, 500, 999]
+    del junk
+
+
 def test_host_only_context_refuses_device_work():
     ctx = _lib.Context(-1)
     out = np.zeros(1)
