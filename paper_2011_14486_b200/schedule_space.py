@@ -129,6 +129,18 @@ class _PipelineInfo:
         for st in self.stages:
             cons = cmap[st.name]
             self.sole.append(cons[0] if len(cons) == 1 else None)
+        # the native encoder's stage table (csrc/hostenc.c): per schedule
+        # index (name, pure dims, reduction dims, sole consumer), None where
+        # two loop names could coincide (those stages take the Python path)
+        stab = []
+        for st, sole in zip(self.stages, self.sole):
+            pure = tuple(n for n, _ in st.dims)
+            red = tuple(n for n, _ in st.reduction_dims)
+            names = [*pure, *(n + "o" for n in pure), *(n + "i" for n in pure), *red]
+            ok = (len(set(names)) == len(names) and 1 <= len(pure) <= 4 and len(red) <= 4
+                  and all(isinstance(n, str) for n in names))
+            stab.append((st.name, pure, red, sole) if ok else None)
+        self.stab = tuple(stab)
         self.enc_cache = {}   # id(decision) -> (decision, bytes, schedule index)
         # (schedule index, decision) -> bytes: decisions are frozen dataclasses,
         # so equal decisions built by any caller (a foreign search's own
@@ -304,7 +316,7 @@ def encode_states(states):
         inf = _info(p)
         if _hostenc is not None:  # native: one C call per group (csrc/hostenc.c)
             try:
-                rb, ob = _hostenc.encode_group(states, idxs, inf.T, inf.encode, inf.val_cache)
+                rb, ob = _hostenc.encode_group(states, idxs, inf.T, inf.encode, inf.val_cache, inf.stab)
             except ValueError as e:
                 raise IllegalActionError(str(e)) from None
             recs = np.frombuffer(rb, dtype=_lib.DECISION_DTYPE)

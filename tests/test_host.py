@@ -79,6 +79,72 @@ def test_candidates_match_golden(candidates_golden, greedy_golden):
             s = ss.apply(s, c[r5.randrange(len(c))])
 
 
+def _fresh(d, **kw):
+    """A new decision object equal to d (or with fields replaced)."""
+    import dataclasses
+    return dataclasses.replace(d, **kw)
+
+
+def test_native_encoder_matches_python(candidates_golden, greedy_golden):
+    """csrc/hostenc.c's encode_native against _PipelineInfo._encode_fields on
+    every candidate of the golden walks (fresh objects, empty caches: no
+    call may reach the Python encoder), and every illegal mutation going to
+    the Python encoder and raising its error."""
+    from paper_2011_14486_b200 import _hostenc
+    n_legal = n_bad = 0
+    for key, walk in candidates_golden.items():
+        p = pipeline_from(greedy_golden[key])
+        inf = ss._info(p)
+        s = ss.initial_state(p)
+        r5 = __import__("oracle").SplitMix(5)
+        for _ in walk:
+            j = len(s.decisions)
+            cands = ss.candidate_actions(s)
+            calls = []
+
+            def fallback(idx, d):
+                calls.append(idx)
+                return inf.encode(idx, d)
+
+            children = [ss.ScheduleState(p, (*s.decisions, _fresh(a))) for a in cands]
+            _hostenc.clear()
+            rb, _ = _hostenc.encode_group(children, list(range(len(children))), inf.T, fallback, {}, inf.stab)
+            want = b"".join(b"".join(inf._encode_fields(i, d) for i, d in enumerate(c.decisions))
+                            for c in children)
+            assert rb == want, key
+            if inf.stab[j] is not None:
+                assert not calls, (key, j)
+            n_legal += len(children)
+            a = cands[0]
+            st = inf.stages[j]
+            bad = [_fresh(a, stage=a.stage + "_x"), _fresh(a, vectorize_width=0),
+                   _fresh(a, vectorize_width=256), _fresh(a, order=a.order[:-1]),
+                   _fresh(a, order=(*a.order[:-1], a.order[0])), _fresh(a, splits=((st.dims[0][0], 1),)),
+                   _fresh(a, splits=((st.dims[0][0], 256),)), _fresh(a, splits=(("nope", 2),)),
+                   _fresh(a, compute_at=("nope", 0)), _fresh(a, store_at=("nope", 1))]
+            if a.compute_at is not None:
+                bad += [_fresh(a, compute_at=(a.compute_at[0], 8)),
+                        _fresh(a, store_at=(a.compute_at[0], a.compute_at[1] + 1))]
+            for d in bad:
+                child = ss.ScheduleState(p, (*s.decisions, d))
+                try:
+                    inf._encode_fields(j, d)
+                    want_err = None
+                except Exception as e:  # the reference's error for this decision
+                    want_err = (type(e), str(e))
+                _hostenc.clear()
+                if want_err is None:  # a mutation that is still legal
+                    rb, _ = _hostenc.encode_group([child], [0], inf.T, inf.encode, {}, inf.stab)
+                    assert rb[-16:] == inf._encode_fields(j, d)
+                    continue
+                with pytest.raises(want_err[0]) as ei:
+                    _hostenc.encode_group([child], [0], inf.T, inf.encode, {}, inf.stab)
+                assert str(ei.value) == want_err[1]
+                n_bad += 1
+            s = ss.apply(s, cands[r5.randrange(len(cands))])
+    assert n_legal > 1000 and n_bad > 100, (n_legal, n_bad)
+
+
 def test_encode_decode_roundtrip(state_sets):
     for name, z in state_sets.items():
         p = pipeline_from(z)
