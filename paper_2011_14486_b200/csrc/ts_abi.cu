@@ -1557,7 +1557,12 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   int* gticket = nullptr;
   if (fused_layers) {
     const size_t hb = sizeof(unsigned long long) * (size_t)T * kMaxChildren;
-    TS_CUDA(ctx->ghash.reserve(hb + sizeof(int) * (size_t)(T + 1), ctx->stream));
+    // sized for the largest pipeline on first use (16.8 MB): growing it per
+    // new, longer pipeline cost a cudaFree + cudaMalloc (0.8-4 ms measured
+    // after the bench's training leg) inside that pipeline's first call
+    TS_CUDA(ctx->ghash.reserve(sizeof(unsigned long long) * (size_t)TS_MAX_STAGES * kMaxChildren +
+                                   sizeof(int) * (size_t)(TS_MAX_STAGES + 1),
+                               ctx->stream));
     ghash = ctx->ghash.as<unsigned long long>();
     gcount = reinterpret_cast<int*>(ctx->ghash.as<char>() + hb);
     gticket = gcount + T;
@@ -1569,7 +1574,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   // device state rows start as the all-unscheduled normalized matrix
   // device state: rows (all-unscheduled normalized matrix to start), then
   // b + x.Wx per scheduled row (H = 32; written as each winner is installed)
-  TS_CUDA(ctx->tmp.reserve(sizeof(double) * T * (F + 128)));
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * TS_MAX_STAGES * (F + 128), ctx->stream));  // (max: see ghash)
   double* state_rows = ctx->tmp.as<double>();
   double* zx_state = state_rows + (int64_t)T * F;
   TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
