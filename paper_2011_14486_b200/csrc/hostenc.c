@@ -240,6 +240,20 @@ static int encode_native(PyObject* const* f, PyObject* ent, uint8_t* out) {
   return 1;
 }
 
+/* identity slot for d (held: its pointer stays valid while cached) */
+static void remember(PyObject* d, int j, PyObject* vcache, const uint8_t* rec) {
+  if (used >= CAP / 2) table_clear(); /* bounded: foreign callers bring new objects */
+  size_t s = slot_of(d, vcache);
+  while (table[s].obj) s = (s + 1) & (CAP - 1);
+  Py_INCREF(d);
+  Py_INCREF(vcache);
+  table[s].obj = d;
+  table[s].owner = vcache;
+  table[s].idx = j;
+  memcpy(table[s].rec, rec, 16);
+  ++used;
+}
+
 /* record of decision d at schedule index j of the pipeline whose value dict
  * is vcache: table hit, native encoding, value hit or Python fallback */
 static int record_of(PyObject* d, int j, PyObject* fallback, PyObject* vcache, PyObject* stab, uint8_t* out) {
@@ -267,7 +281,10 @@ static int record_of(PyObject* d, int j, PyObject* fallback, PyObject* vcache, P
     if (nf == 7) ok = encode_native(f, PyTuple_GET_ITEM(stab, j), out);
     for (int q = 0; q < nf; ++q) Py_DECREF(f[q]);
     if (ok < 0) return -1;
-    if (ok) goto remember;
+    if (ok) {
+      remember(d, j, vcache, out);
+      return 0;
+    }
   }
   PyObject* jj = PyLong_FromLong(j); /* a cached small int */
   if (!jj) return -1;
@@ -315,17 +332,7 @@ static int record_of(PyObject* d, int j, PyObject* fallback, PyObject* vcache, P
   }
   memcpy(out, PyBytes_AS_STRING(r), 16);
   Py_DECREF(r);
-remember:
-  if (used >= CAP / 2) table_clear(); /* bounded: foreign callers bring new objects */
-  s = slot_of(d, vcache);
-  while (table[s].obj) s = (s + 1) & (CAP - 1);
-  Py_INCREF(d);
-  Py_INCREF(vcache);
-  table[s].obj = d;
-  table[s].owner = vcache;
-  table[s].idx = j;
-  memcpy(table[s].rec, out, 16);
-  ++used;
+  remember(d, j, vcache, out);
   return 0;
 }
 
