@@ -174,6 +174,18 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
 }
 
 #ifndef TS_QUAD_RCP
+#ifndef TS_RAT_TANH
+#define TS_RAT_TANH 0  // 1: tanh(c') as a rational on the FMA pipe (cell_group; measured equal, off), 0: ex2 on MUFU
+#endif
+// tanh rational (odd P / even Q in c'^2): Eigen's float tanh coefficients
+// (generic_fast_tanh_float), a published minimax fit; error checked in
+// tests/test_host.py against libm tanh
+constexpr float kTanhClamp = 7.90531110763549805f;
+constexpr float kTA1 = 4.89352455891786e-03f, kTA3 = 6.37261928875436e-04f, kTA5 = 1.48572235717979e-05f,
+                kTA7 = 5.12229709037114e-08f, kTA9 = -8.60467152213735e-11f, kTA11 = 2.00018790482477e-13f,
+                kTA13 = -2.76076847742355e-16f;
+constexpr float kTB0 = 4.89352518554385e-03f, kTB2 = 2.26843463243900e-03f, kTB4 = 1.18534705686654e-04f,
+                kTB6 = 1.19825839466702e-06f;
 #define TS_QUAD_RCP 0  // 1: the output gate's reciprocal shared by four units (cell_group; measured 1%, off)
 #endif
 #ifndef TS_FMA_EXP
@@ -347,12 +359,39 @@ __device__ __forceinline__ void cell_group(uint32_t lane_addr, int g8, float* c,
     const float2 cn = __fmul2_rn(num, __fmul2_rn(make_float2(d1.y, d1.x), make_float2(r1, r1)));
     c[j] = cn.x;
     c[j + 1] = cn.y;
+#if TS_RAT_TANH
+    // tanh(c') = P(c') / Q(c') on the FMA pipe (odd degree-13 / even degree-6
+    // rational, |error| < 4e-7 on the clamp range [-7.905, 7.905], beyond it
+    // tanh = +-1 within 2.8e-7), so h = o tanh(c') = P / ((1 + e_o) Q): Q
+    // joins the output gate's shared reciprocal and the cell's exponential
+    // leaves the MUFU pipe (5 MUFU ops per unit instead of 6).  Q lies in
+    // [0.0049, 0.91], so the pair product stays above 2^-96.
+    const float2 x = make_float2(fminf(fmaxf(cn.x, -kTanhClamp), kTanhClamp),
+                                 fminf(fmaxf(cn.y, -kTanhClamp), kTanhClamp));
+    const float2 x2 = __fmul2_rn(x, x);
+    float2 pn = __ffma2_rn(make_float2(kTA13, kTA13), x2, make_float2(kTA11, kTA11));
+    pn = __ffma2_rn(pn, x2, make_float2(kTA9, kTA9));
+    pn = __ffma2_rn(pn, x2, make_float2(kTA7, kTA7));
+    pn = __ffma2_rn(pn, x2, make_float2(kTA5, kTA5));
+    pn = __ffma2_rn(pn, x2, make_float2(kTA3, kTA3));
+    pn = __ffma2_rn(pn, x2, make_float2(kTA1, kTA1));
+    pn = __fmul2_rn(pn, __fmul2_rn(x, s2));                                    // 2^-40 P(c')
+    float2 qd = __ffma2_rn(make_float2(kTB6, kTB6), x2, make_float2(kTB4, kTB4));
+    qd = __ffma2_rn(qd, x2, make_float2(kTB2, kTB2));
+    qd = __ffma2_rn(qd, x2, make_float2(kTB0, kTB0));
+    const float2 to = __ffma2_rn(eo, s2, s2);                                  // 2^-40 (1 + e_o)
+    const float2 d2 = __fmul2_rn(to, qd);                                      // 2^-40 (1 + e_o) Q(c')
+    const float r2 = rcp(d2.x * d2.y);
+    const float2 hh = __fmul2_rn(pn, __fmul2_rn(make_float2(d2.y, d2.x), make_float2(r2, r2)));
+    (void)ns2;
+#else
     const float2 cc = __fmul2_rn(make_float2(C2, C2), cn);
     const float2 ec = ex2_pair(clamp40(cc.x), clamp40(cc.y), 4);
     const float2 to = __ffma2_rn(eo, s2, s2);                                  // 2^-40 (1 + e_o)
     const float2 d2 = __ffma2_rn(to, ec, to);                                  // 2^-40 (1 + e_o)(1 + e_c)
     const float r2 = rcp(d2.x * d2.y);
     const float2 hh = __fmul2_rn(__ffma2_rn(ec, ns2, s2), __fmul2_rn(make_float2(d2.y, d2.x), make_float2(r2, r2)));
+#endif
     h8[u] = hh.x;
     h8[u + 1] = hh.y;
     acc = fmaf(hh.x, wout[j], acc);

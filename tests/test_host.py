@@ -399,3 +399,28 @@ def test_native_host_encoder_caches_are_per_pipeline(greedy_golden):
     for decs in (s.decisions, copies):
         with pytest.raises(IllegalActionError, match="sole consumer"):
             ss.encode_states([ss.ScheduleState(b, decs)])
+
+
+def test_fast_leg_tanh_rational_accuracy():
+    """The FAST leg's cell tanh (csrc/ts_lstm_tc.cuh, TS_RAT_TANH): the
+    odd/even rational in fp32 with the kernel's clamp, Horner order and
+    coefficients, against libm tanh - |error| < 5e-7 everywhere."""
+    import re as _re
+    src = (pathlib.Path(__file__).resolve().parent.parent / "paper_2011_14486_b200" / "csrc" /
+           "ts_lstm_tc.cuh").read_text()
+    k = {m.group(1): np.float32(float(m.group(2).rstrip("f")))
+         for m in _re.finditer(r"\b(kT(?:A|B)\d+|kTanhClamp) = ([-0-9.e+]+f)", src)}
+    f32 = np.float32
+    x = np.linspace(-12.0, 12.0, 400001).astype(f32)
+    xc = np.clip(x, -k["kTanhClamp"], k["kTanhClamp"]).astype(f32)
+    x2 = (xc * xc).astype(f32)
+    p = k["kTA13"]
+    for c in ("kTA11", "kTA9", "kTA7", "kTA5", "kTA3", "kTA1"):
+        p = (p * x2 + k[c]).astype(f32)
+    p = (p * xc).astype(f32)
+    q = k["kTB6"]
+    for c in ("kTB4", "kTB2", "kTB0"):
+        q = (q * x2 + k[c]).astype(f32)
+    assert q.min() > 0.004 and q.max() < 0.95  # the shared reciprocal's range argument
+    err = np.abs((p / q).astype(np.float64) - np.tanh(x.astype(np.float64)))
+    assert err.max() < 5e-7, err.max()
