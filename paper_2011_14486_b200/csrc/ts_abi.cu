@@ -48,7 +48,13 @@ struct DevBuf {
   }
   cudaError_t reserve(size_t n) {
     if (n <= bytes) return cudaSuccess;
-    if (p) cudaFree(p);
+    // growth: work queued on any of the context's streams may still read the
+    // old buffer; wait for the device explicitly rather than relying on
+    // cudaFree's implicit synchronization
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
     cudaError_t e = cudaMalloc(&p, n);
@@ -179,6 +185,14 @@ struct ts_ctx {
   int64_t greedy_visited = 0;
   bool tr_group_attr_set = false;
 };
+
+// fused greedy: per layer up to this many children; their row hashes for
+// every layer of the largest pipeline plus the per-layer counts and ticket
+constexpr int kGreedyMaxChildren = 4096;
+static size_t greedy_hash_bytes() {
+  return sizeof(unsigned long long) * (size_t)TS_MAX_STAGES * kGreedyMaxChildren +
+         sizeof(int) * (size_t)(TS_MAX_STAGES + 1);
+}
 
 namespace {
 void swap_buf(DevBuf& a, DevBuf& b) {
@@ -492,6 +506,11 @@ int ts_ctx_create(int device, ts_ctx** out) {
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(d_exp_tab, ts_exp_tab_bits, sizeof(uint64_t) * TS_EXP_NTAB);
   if (e == cudaSuccess) e = ctx->status.reserve(sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(ctx->status.p, 0, sizeof(int));
+  // the greedy's scratch (child-row hashes, state rows), sized for the
+  // largest pipeline here: allocated inside a first greedy call it cost
+  // 7-110 ms of cudaMalloc once the device holds the bench's earlier legs
+  if (e == cudaSuccess) e = ctx->ghash.reserve(greedy_hash_bytes());
+  if (e == cudaSuccess) e = ctx->tmp.reserve(sizeof(double) * TS_MAX_STAGES * (F + 128));
   if (e != cudaSuccess) {
     delete ctx;
     return TS_ERR_CUDA;
@@ -1542,13 +1561,25 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   PipelineSlot* P = get_pipe(ctx, pipeline_id);
   if (!P) return fail(ctx, TS_ERR_ARG, "unknown pipeline id");
   TS_CUDA(cudaSetDevice(ctx->device));
+  // TS_GREEDY_TRACE: setup phases (first calls per pipeline) on stderr
+  const bool setup_trace = getenv("TS_GREEDY_TRACE") != nullptr;
+  double t_mark = 0.0;
+  auto mark = [&](const char* what) {
+    if (!setup_trace) return;
+    const double t = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (what) fprintf(stderr, "ts_greedy setup: %s %.0f us\n", what, t - t_mark);
+    t_mark = t;
+  };
+  mark(nullptr);
   int rc = ensure_pipe_ready(ctx, P);
+  mark("pipeline rows and prefix");
   if (rc) return rc;
   TS_CUDA(ctx->gstat.reserve(sizeof(unsigned long long)));
   TS_CUDA(cudaMemsetAsync(ctx->gstat.p, 0, sizeof(unsigned long long), ctx->stream));
+  mark("stats");
   const PipelineDesc& D = *P->h;
   const int T = D.n_stages;
-  constexpr int kMaxChildren = 4096;
+  constexpr int kMaxChildren = kGreedyMaxChildren;
   // fused layers (H = 32): children row hashes per layer for the distinct
   // count, and the layer ticket, zeroed once (each layer's last block re-zeroes it)
   const bool fused_layers = ctx->hidden == 32;
@@ -1557,24 +1588,21 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   int* gticket = nullptr;
   if (fused_layers) {
     const size_t hb = sizeof(unsigned long long) * (size_t)T * kMaxChildren;
-    // sized for the largest pipeline on first use (16.8 MB): growing it per
-    // new, longer pipeline cost a cudaFree + cudaMalloc (0.8-4 ms measured
-    // after the bench's training leg) inside that pipeline's first call
-    TS_CUDA(ctx->ghash.reserve(sizeof(unsigned long long) * (size_t)TS_MAX_STAGES * kMaxChildren +
-                                   sizeof(int) * (size_t)(TS_MAX_STAGES + 1),
-                               ctx->stream));
+    TS_CUDA(ctx->ghash.reserve(greedy_hash_bytes(), ctx->stream));  // (sized at context creation)
     ghash = ctx->ghash.as<unsigned long long>();
     gcount = reinterpret_cast<int*>(ctx->ghash.as<char>() + hb);
     gticket = gcount + T;
     TS_CUDA(cudaMemsetAsync(gcount, 0, sizeof(int) * (size_t)(T + 1), ctx->stream));
   }
+  mark("child-row hashes");
   std::vector<Nest> nests(T);
   std::vector<ts_decision> cands;
   cands.reserve(1024);
   // device state rows start as the all-unscheduled normalized matrix
   // device state: rows (all-unscheduled normalized matrix to start), then
   // b + x.Wx per scheduled row (H = 32; written as each winner is installed)
-  TS_CUDA(ctx->tmp.reserve(sizeof(double) * TS_MAX_STAGES * (F + 128), ctx->stream));  // (max: see ghash)
+  TS_CUDA(ctx->tmp.reserve(sizeof(double) * TS_MAX_STAGES * (F + 128), ctx->stream));  // (sized at context creation)
+  mark("state rows");
   double* state_rows = ctx->tmp.as<double>();
   double* zx_state = state_rows + (int64_t)T * F;
   TS_CUDA(cudaMemcpyAsync(state_rows, P->init_norm.p, sizeof(double) * T * F, cudaMemcpyDeviceToDevice,
@@ -1582,6 +1610,7 @@ int ts_greedy(ts_ctx* ctx, int pipeline_id, double epsilon, uint64_t* rng_state,
   TS_CUDA(ctx->nest.reserve(sizeof(Nest)));
   TS_CUDA(ctx->h_stage.reserve(sizeof(ts_decision) * (4096 + 8)));
   TS_CUDA(ctx->h_out.reserve(sizeof(double) * 4));
+  mark("nest, staging");
   uint64_t rng = rng_state ? *rng_state : 0;
   const bool trace = getenv("TS_GREEDY_TRACE") != nullptr;
   double t_enum = 0.0, t_wait = 0.0;
